@@ -1,0 +1,80 @@
+"""Closed-form space model of the SI, written out as printed.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Units are stored
+elements (one int32 or fp32 each), as the SI counts them.
+
+Readings:
+  * The encoding is stride-agnostic (A15), so the ptr formulas use the
+    stride-1 partition count Ow1 = Wp - K_w + 1 and ceil(K_w/s_w) = K_w.
+  * NOP_size is 3 iff Pad_Left = 0 (VALID) and K_w > 1, else 0 (A2; SI Alg. 5
+    has no NOP block for K_w = 1).
+  * S_im2col uses the actual (floor) output dims (A14); S_MEC uses the padded
+    height (MEC lowers the padded map).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _ow1(d: dict) -> int:
+    return d["W"] + d["pad_left"] + d["pad_right"] - d["S"] + 1
+
+
+def op_size_eq2(d: dict) -> int:
+    """SI Eq. 2: (1+O_w) if K_w = 1, else (ceil(K_w/s_w) - M)(1+O_w),
+    M = max(1, pad_left)."""
+    ow1 = _ow1(d)
+    if d["S"] == 1:
+        return 1 + ow1
+    M = max(1, d["pad_left"])
+    return (d["S"] - M) * (1 + ow1)
+
+
+def nop_size(d: dict) -> int:
+    """NOP block: 3 entries for VALID padding, 0 for SAME."""
+    return 3 if (d["pad_left"] == 0 and d["S"] > 1) else 0
+
+
+def ptr_size_eq3(d: dict, chan_density: np.ndarray, count_npf: int) -> int:
+    """SI Eq. 3:
+    sum_{n,c} max(1, 1[rho_{n,c} > 0] (NOP_size + OP_size)) - count_NPF (O_w - 1)."""
+    per = nop_size(d) + op_size_eq2(d)
+    live = np.asarray(chan_density).reshape(-1) > 0
+    total = int(np.sum(np.maximum(1, live.astype(np.int64) * per)))
+    return total - count_npf * (_ow1(d) - 1)
+
+
+def da_size_eq4(d: dict, chan_density: np.ndarray) -> int:
+    """SI Eq. 4: DA = IN_CPO = I_h I_w sum_{n,c} rho_{n,c}."""
+    return int(round(d["H"] * d["W"] * float(np.sum(chan_density))))
+
+
+def in_cps_size_eq5(census: np.ndarray) -> int:
+    """SI Eq. 5:
+    sum (C'_1 + 2C'_2 + 3C'_3 + 4C'_4 + C''_1 + 2C''_2 + 2C''_3 + 2C''_4)."""
+    c1, c2, c3, c4, d1, d2, d3, d4 = (int(v) for v in census)
+    return c1 + 2 * c2 + 3 * c3 + 4 * c4 + d1 + 2 * d2 + 2 * d3 + 2 * d4
+
+
+def _out(i, p0, p1, k, s):
+    return (i + p0 + p1 - k) // s + 1
+
+
+def S_im2col(d: dict) -> int:
+    """SI Eq. 6: I_n O_w O_h I_c K_w K_h."""
+    Oh = _out(d["H"], d["pad_top"], d["pad_bottom"], d["R"], d["stride_h"])
+    Ow = _out(d["W"], d["pad_left"], d["pad_right"], d["S"], d["stride_w"])
+    return d["N"] * Ow * Oh * d["C"] * d["S"] * d["R"]
+
+
+def S_mec(d: dict) -> int:
+    """SI Eq. 11: I_n O_w K_w I_h I_c (I_h of the padded map)."""
+    Ow = _out(d["W"], d["pad_left"], d["pad_right"], d["S"], d["stride_w"])
+    Hp = d["H"] + d["pad_top"] + d["pad_bottom"]
+    return d["N"] * Ow * d["S"] * Hp * d["C"]
+
+
+def channel_density(x: np.ndarray) -> np.ndarray:
+    """rho_{n,c}: fraction of NZEs in each channel plane."""
+    N, C, H, W = x.shape
+    return (x.reshape(N, C, H * W) != 0).sum(axis=2) / float(H * W)
