@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the CPO/CPS sparse-conv hot path on B200 (contract: see DESIGN.md §Measurement).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2]
+
+One step = one pass of the hot path over one batch of the workload: CPO encode
+(one launch) + sparse convolution (one launch) of configs[1] (cfg2: 1x64x56x56,
+rho 0.3, 64 output channels, 3x3, s1, pad 1).  Inputs are synthetic (seeded
+clustered-ReLU, DESIGN.md §Input recipe) and resident in HBM; L2 is flushed
+between timed steps.  value = dense-equivalent GFLOP/s (2*N*K*C*R*S*Oh*Ow per
+step / device time), summed over ranks (weak scaling: every rank encodes and
+convolves its own batch; no data-path collective).  The same line carries the
+CPS path, the im2col baseline (lowering + GEMM), the compression ratio, the
+roofline of the dominant kernel, the host-buffer end-to-end number, clocks and
+the oracle timed on the host (cpu_baseline).
+
+--impl reference runs the CPU oracle (oracle/, plain C, FP64) as the reference
+arm on the same workload, on the host, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, cfg5_layers, clustered_relu, he_normal  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT, FP32_LANES, FALLBACK_HBM = 148, 128, 6650.0
+
+
+def workload(name: str):
+    if name.startswith("cfg5"):
+        layer = cfg5_layers(batch=32)[int(name.split("L")[-1])]
+        return layer
+    return CONFIGS[name]
+
+
+def dense_flops(d, Oh, Ow):
+    return 2.0 * d["N"] * d["K"] * d["C"] * d["R"] * d["S"] * Oh * Ow
+
+
+def nze_macs(d, x: np.ndarray, Oh, Ow) -> int:
+    """Exact multiply-adds of the sparse conv: for each NZE, the (output, tap) pairs
+    that see it (rows x cols, stride-aware), times K.  Measurement accounting only."""
+    Hp, Wp = d["H"] + d["pad_top"] + d["pad_bottom"], d["W"] + d["pad_left"] + d["pad_right"]
+
+    def cov(n_in, k, s, n_out):
+        c = np.zeros(n_in, dtype=np.int64)
+        for h in range(n_in):
+            c[h] = sum(1 for l in range(k) if h - l >= 0 and (h - l) % s == 0 and (h - l) // s < n_out)
+        return c
+    ch = cov(Hp, d["R"], d["stride_h"], Oh)[d["pad_top"]:d["pad_top"] + d["H"]]
+    cw = cov(Wp, d["S"], d["stride_w"], Ow)[d["pad_left"]:d["pad_left"] + d["W"]]
+    nz = (x != 0).sum(axis=(0, 1)).astype(np.int64)      # [H, W]
+    return int(ch @ nz @ cw) * d["K"]
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, 1965.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU oracle legs
+
+def oracle_time(d, x, w, budget_s: float, cps: bool = False):
+    """Oracle encode + sparse conv (Alg. 1/2 or 3/4, single-threaded C) on a bounded
+    sample: as many images of the batch as fit the budget (at least one)."""
+    import oracle
+    oracle.build()
+    t_used, n_done, flops = 0.0, 0, 0.0
+    Oh, Ow = oracle.out_hw(d)
+    d1 = dict(d, N=1)
+    while n_done < d["N"] and (n_done == 0 or t_used < budget_s):
+        xi = x[n_done:n_done + 1]
+        t0 = time.perf_counter()
+        enc = oracle.encode(d1, xi, cps=cps)
+        oracle.sparse_conv(d1, enc, w)
+        t_used += time.perf_counter() - t0
+        flops += dense_flops(d1, Oh, Ow)
+        n_done += 1
+    return t_used, n_done, flops
+
+
+def run_reference(args):
+    """--impl reference: the oracle as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c = workload(args.workload)
+    d = c["desc"]
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"], c["dead_frac"], c["zero_tile_frac"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    for _ in range(args.warmup):
+        oracle_time(d, x[:1], w, 0.0)
+    tot_t, tot_f, imgs = 0.0, 0.0, 0
+    for _ in range(args.steps):
+        t, n, f = oracle_time(d, x, w, budget_s=20.0 / max(1, args.steps))
+        tot_t, tot_f, imgs = tot_t + t, tot_f + f, imgs + n
+    val = tot_f / tot_t / 1e9
+    line = {"impl": "reference", "metric": "dense-equivalent GFLOP/s of CPO encode + sparse conv (per layer)",
+            "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"]},
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{imgs} image(s) of {args.workload} over {args.steps} steps"},
+            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- GPU leg
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_08314_b200 as spc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    c = workload(args.workload)
+    d = c["desc"]
+    # each rank draws its own images (weak scaling: independent batches)
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"] + 7919 * rank, c["dead_frac"],
+                       c["zero_tile_frac"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    Oh, Ow = spc.out_hw(d)
+    xg = torch.from_numpy(x).to(dev)
+    wg = torch.from_numpy(w).to(dev)
+    wp = torch.empty_like(wg).reshape(-1)
+    spc.spc_pack_weights(d, wg, wp)
+    enc = spc.alloc_encoding(d, device=dev)
+    enc_s = spc.alloc_encoding(d, device=dev)
+    ws = spc.alloc_workspace(d, device=dev)
+    y = torch.empty((d["N"], d["K"], Oh, Ow), device=dev)
+    lowered = torch.empty(d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow, device=dev)
+    flush = torch.empty(int(2 * 128 * 2 ** 20) // 4, dtype=torch.float32, device=dev)  # > 2x L2
+
+    def step_cpo(e0=None, e1=None, e2=None):
+        if e0 is not None: e0.record(stream)
+        spc.cpo_encode(d, xg, enc, ws)
+        if e1 is not None: e1.record(stream)
+        spc.sparse_conv_forward(d, enc, wp, y, False, ws)
+        if e2 is not None: e2.record(stream)
+
+    def step_cps(e0=None, e1=None, e2=None):
+        if e0 is not None: e0.record(stream)
+        spc.cps_encode(d, xg, enc_s, ws)
+        if e1 is not None: e1.record(stream)
+        spc.sparse_conv_forward(d, enc_s, wp, y, False, ws)
+        if e2 is not None: e2.record(stream)
+
+    def step_im2col(e0=None, e1=None, e2=None):
+        if e0 is not None: e0.record(stream)
+        spc.im2col_conv_forward(d, xg, wg, y, False, lowered)
+        if e2 is not None: e2.record(stream)
+
+    def timed(fn, steps, warmup, split=True):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()                      # L2 flush between timed steps (outside the events)
+            fn(*ev[i])
+        torch.cuda.synchronize()
+        tot = [e[0].elapsed_time(e[2]) for e in ev]
+        first = [e[0].elapsed_time(e[1]) for e in ev] if split else [0.0] * steps
+        return sum(tot), sum(first)
+
+    # --- main timed region (CPO path), barrier + sync on both sides, max over ranks
+    for _ in range(args.warmup):
+        step_cpo()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        t_ms, t_enc_ms = timed(step_cpo, args.steps, 0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_conv_ms = t_ms - t_enc_ms
+    tmax = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tmax = float(tt.item())
+    flops_step = dense_flops(d, Oh, Ow)
+    value = flops_step * args.steps * world / (tmax * 1e-3) / 1e9
+
+    # --- side measurements (same process, rank 0 reports)
+    t_cps, t_cps_enc = timed(step_cps, args.steps, 1)
+    t_i2c, _ = timed(step_im2col, args.steps, 1, split=False)
+
+    # encoding sizes, CR (paper units: elements of ptr + DA + IN vs S_im2col)
+    pl_, dl_, il_ = spc.spc_encoding_lengths(enc)
+    ps_, ds_, is_ = spc.spc_encoding_lengths(enc_s)
+    s_im2col = d["N"] * Oh * Ow * d["C"] * d["R"] * d["S"]
+    side = 3 * (d["N"] * d["C"] + 1) * 2   # int64 side tables in 4-byte elements
+    cr_cpo = s_im2col / (pl_ + dl_ + il_)
+    cr_cps = s_im2col / (ps_ + ds_ + is_)
+
+    # --- roofline of the dominant kernel (measured per-launch averages)
+    hbm_gbs, sm_max_mhz, peak_src = load_peaks()
+    p_fp32 = SM_COUNT * FP32_LANES * 2 * sm_max_mhz * 1e6 / 1e12   # TFLOP/s, derived
+    macs = nze_macs(d, x, Oh, Ow)
+    conv_bytes = 4 * (pl_ + dl_ + il_) + 8 * 2 * (d["N"] * d["C"] + 1) + 4 * wg.numel() + 4 * y.numel()
+    enc_bytes = 4 * xg.numel() + 4 * (pl_ + dl_ + il_) + 8 * 3 * (d["N"] * d["C"] + 1)
+    conv_s = t_conv_ms / args.steps * 1e-3
+    enc_s = t_enc_ms / args.steps * 1e-3
+    conv_flops = 2.0 * macs
+    t_roof_conv = max(conv_bytes / (hbm_gbs * 1e9), conv_flops / (p_fp32 * 1e12))
+    conv_bound = "alu" if conv_flops / (p_fp32 * 1e12) >= conv_bytes / (hbm_gbs * 1e9) else "hbm"
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.workload, {}).get("sparse_conv")
+        except Exception:
+            traffic = None
+    if conv_s >= enc_s:
+        if conv_bound == "alu":
+            roof = {"kernel": "sparse_conv_kernel", "bound": "alu", "achieved": conv_flops / conv_s / 1e12,
+                    "peak": p_fp32, "unit": "TFLOP/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
+                    "algorithmic_flops": conv_flops, "algorithmic_bytes": conv_bytes}
+        else:
+            roof = {"kernel": "sparse_conv_kernel", "bound": "hbm", "achieved": conv_bytes / conv_s / 1e9,
+                    "peak": hbm_gbs, "unit": "GB/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
+                    "peak_source": peak_src, "algorithmic_bytes": conv_bytes}
+    else:
+        roof = {"kernel": "encode_kernel", "bound": "hbm", "achieved": enc_bytes / enc_s / 1e9, "peak": hbm_gbs,
+                "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs, "traffic": None,
+                "peak_source": peak_src, "algorithmic_bytes": enc_bytes}
+
+    # --- end to end through the public API with host buffers (pinned), copies in the timed region
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty(y.shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        xg.copy_(xh, non_blocking=True); step_cpo(); yh.copy_(y, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        e0.record(stream)
+        xg.copy_(xh, non_blocking=True)
+        step_cpo()
+        yh.copy_(y, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = flops_step * args.steps * world / (e2e_ms * 1e-3) / 1e9
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        t, n, f = oracle_time(d, x, w, budget_s=args.cpu_budget)
+        cpu = {"value": f / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n} image(s) of {args.workload}: oracle CPO encode + Alg. 2 conv, single thread, FP64"}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        us = lambda ms: 1e3 * ms / args.steps  # noqa: E731
+        line = {
+            "metric": "dense-equivalent GFLOP/s of CPO encode + sparse conv (per layer), vs GPU im2col",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"],
+                       "dead_frac": c["dead_frac"], "zero_tile_frac": c["zero_tile_frac"],
+                       "l2": "flushed between timed steps (256 MiB write)", "global_batch": d["N"] * world},
+            "layer_us": {"cpo_encode": us(t_enc_ms), "cpo_conv": us(t_conv_ms), "cpo_total": us(t_ms),
+                         "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
+                         "im2col_total": us(t_i2c)},
+            "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
+                       "gemm": "SIMT FP32 FFMA (tile 128x128)"},
+            "speedup_vs_im2col": t_i2c / t_ms,
+            "cr": {"cpo": cr_cpo, "cps": cr_cps, "cpo_with_side_tables": s_im2col / (pl_ + dl_ + il_ + side),
+                   "ptr": pl_, "da": dl_, "in_cpo": il_, "in_cps": is_, "S_im2col": s_im2col},
+            "nze_macs": macs, "density_measured": float((x != 0).mean()),
+            "roofline": roof,
+            "roofline_encode": {"bound": "hbm", "achieved": enc_bytes / enc_s / 1e9, "peak": hbm_gbs,
+                                "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs},
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": int(4 * xg.numel()),
+                    "d2h_bytes_per_step": int(4 * y.numel())},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "version": spc.spc_version(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * spconv.h -- C ABI of the B200 (sm_100a) implementation of the hot path of
+ * arXiv 2104.08314, "High Performance Convolution Using Sparsity and Patterns
+ * for Inference in Deep Convolutional Neural Networks" (CPO / CPS).
+ *
+ * Citations "PAPER.md:<line>" point into the paper text; "reading Ax" points
+ * to DESIGN.md §Readings (the canonical resolution of ambiguous passages).
+ *
+ * Conventions for every entry point
+ *  - Tensor pointers are DEVICE pointers unless the argument says "host".
+ *    The caller owns and allocates every buffer; no call allocates or frees
+ *    device memory.  Device buffers must be 16-byte aligned.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) unless documented as synchronising.
+ *  - Host-side validation happens before any launch; on a non-OK status no
+ *    kernel was launched (except SPC_ECUDA, which reports a launch/runtime
+ *    error).  spc_last_error() returns a thread-local message.
+ *  - Layouts: activations x are NCHW fp32; weights w are KCRS fp32
+ *    (K output channels, C input channels, R = K_h rows, S = K_w columns);
+ *    outputs y are NKHW fp32 with Oh = floor((H+pt+pb-R)/sh)+1 and
+ *    Ow = floor((W+pl+pr-S)/sw)+1 (reading A14).
+ *  - Thread safety: calls on different streams with disjoint buffers and
+ *    workspaces may run concurrently.
+ */
+#ifndef SPCONV_H
+#define SPCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPC_OK = 0,
+    SPC_EINVAL = -1,        /* bad argument: null pointer, shape mismatch, bad capacity */
+    SPC_EUNSUPPORTED = -2,  /* geometry outside the method's scope (see cpo_encode) */
+    SPC_ECAPACITY = -3,     /* a stream capacity was too small (reported by spc_encoding_lengths) */
+    SPC_ECUDA = -4,         /* CUDA launch or runtime error */
+    SPC_ECORRUPT = -5       /* an encoding failed validation */
+} spc_status;
+
+typedef enum { SPC_ALGO_IM2COL = 0, SPC_ALGO_CPO = 1, SPC_ALGO_CPS = 2 } spc_algo;
+
+/* Hybrid selection modes: favour time = argmin{im2col, CPO};
+ * favour space = argmin{im2col, CPS}; best of three = argmin over all three. */
+typedef enum { SPC_FAVOUR_TIME = 0, SPC_FAVOUR_SPACE = 1, SPC_BEST_OF_THREE = 2 } spc_mode;
+
+/* Reserved ptr sentinels (reading A7): NPC = all-zero channel, NPF = all-zero
+ * overlap region.  -1 keeps the meaning "partition owns no
+ * column of this overlap type" (reading A5). */
+#define SPC_NPC ((int32_t)INT32_MIN)
+#define SPC_NPF ((int32_t)(INT32_MIN + 1))
+
+/* The paper's problem statement (Table 1): input
+ * I_n x I_c x I_h x I_w (here N, C, H, W), kernel K x I_c x K_h x K_w
+ * (K, C, R, S), strides s_h, s_w and zero padding. */
+typedef struct {
+    int32_t N, C, H, W;
+    int32_t K, R, S;
+    int32_t stride_h, stride_w;
+    int32_t pad_top, pad_bottom, pad_left, pad_right;
+} spc_conv_desc;
+
+/* One encoded activation tensor (CPO or CPS).  Streams:
+ *   ptr  int32  per channel: NPC, or the blocks NOP [0,a,a+b] (iff pad_left
+ *               = 0), then for t = max(1,pad_left) .. S-1: [t+1, NPF] or
+ *               [t+1, c_0 .. c_{Ow1-1}] with block-relative cumulative NZE
+ *               counts per partition (-1 = no column); for S = 1 a single
+ *               block [0, c_0 .. c_{Ow1-1}] (SI Alg. 5).  Ow1 = Wp - S + 1.
+ *   da   fp32   NZE values, bit copies of x, column-major per block
+ *   in   int32  CPO: row-major local index L + h*S (h in the
+ *               padded frame); CPS: as CPO except the overlapK_w block, which
+ *               holds {first NZE index, 4-bit pattern} per set4 with >= 3
+ *               NZEs and negated indices otherwise
+ * Channels are concatenated n-major then c (reading A19).  The side tables
+ * chan_*_off (GPU-only, not part of the paper's streams or its CR) hold the
+ * exclusive prefix offsets of each (n,c) segment, N*C+1 entries each.
+ * `lengths` (device int64[4]) receives {ptr_len, da_len, in_len, overflow}
+ * at the end of an encode; overflow != 0 means some capacity was too small
+ * and the streams are incomplete.  `algo` and `geom` are written by the
+ * encoder (host fields). */
+typedef struct {
+    int32_t *ptr;  int64_t ptr_cap;
+    float   *da;   int64_t da_cap;
+    int32_t *in;   int64_t in_cap;
+    int64_t *chan_ptr_off, *chan_nz_off, *chan_in_off;
+    int64_t *lengths;
+    int32_t algo;
+    spc_conv_desc geom;
+} spc_encoding;
+
+/* Host.  Worst-case stream capacities for `d` (dense map) and the workspace
+ * bytes every other call below needs at most for this geometry:
+ *   ptr <= N*C*(3 + (S-1)*(1+Ow1)) (S > 1) or N*C*(1+Ow1) (S = 1);
+ *   da  <= N*C*H*W (pad cells are never NZEs);  in <= da.
+ * Returns SPC_EUNSUPPORTED for geometries the encoder rejects. */
+spc_status spc_encode_capacity(const spc_conv_desc *d, int64_t *ptr_cap, int64_t *da_cap,
+                               int64_t *in_cap, size_t *ws_bytes);
+
+/* Host, synchronous.  Zero a workspace once after allocation.  Encoders leave
+ * their scratch state zeroed when they complete, so this is needed only once. */
+spc_status spc_workspace_init(void *ws, size_t ws_bytes, void *stream);
+
+/* CPO encoding (Alg. 1; SI Alg. 5 for S = 1)
+ * of x (device, N*C*H*W fp32) into `out`.  The encoding depends only on x,
+ * R, S and the pads, never on the stride or K (reading A15).  One launch.
+ * Unsupported (SPC_EUNSUPPORTED): R = S = 1 (pointwise);
+ * S > 1 with pad_left != pad_right or pad_left > S-1 or Wp < 2S-1; S = 1 with
+ * horizontal padding; pad_top or pad_bottom > R-1; a plane larger than the
+ * encoder's shared-memory stage (H*W*4 > 200 KB).
+ * ws: >= ws_bytes from spc_encode_capacity, zeroed once (spc_workspace_init). */
+spc_status cpo_encode(const spc_conv_desc *d, const float *x, spc_encoding *out, void *ws,
+                      size_t ws_bytes, void *stream);
+
+/* CPS encoding (Alg. 3): ptr and da identical to CPO; the
+ * overlapK_w block of `in` is pattern-compressed in sets of 4 padded rows
+ * anchored at row 0 (readings A9-A12).  For S = 1 CPS equals CPO (reading
+ * A13).  Same arguments and errors as cpo_encode. */
+spc_status cps_encode(const spc_conv_desc *d, const float *x, spc_encoding *out, void *ws,
+                      size_t ws_bytes, void *stream);
+
+/* Offline, once per layer: repack KCRS weights into [C][R][S][K] so that a
+ * warp's lanes read consecutive output channels (w_packed: C*R*S*K fp32). */
+spc_status spc_pack_weights(const spc_conv_desc *d, const float *w_kcrs, float *w_packed, void *stream);
+
+/* Sparse convolution over an encoding (Alg. 2 CPO / Alg. 4 CPS / SI Alg. 6,
+ * PAPER.md:236-309, :376-426, :1395-1435): y = conv(decode(enc), w) in fp32
+ * with any stride (reading A15, DESIGN.md A.7).  All-zero channels (NPC) and
+ * regions (NPF) are skipped.  fuse_relu != 0 applies max(0, .) to y.
+ * For a CPS encoding the pattern sets are expanded into ws first.
+ * ws: >= ws_bytes from spc_encode_capacity (may be NULL for CPO). */
+spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
+                               float *y, int32_t fuse_relu, void *ws, size_t ws_bytes, void *stream);
+
+/* Dense baseline: im2col lowering of x into ws_lowered as
+ * [N][C*R*S][Oh*Ow] fp32 (SI Eq. 6 elements), then a GEMM per image
+ * y[n] = W[K x CRS] * L[n].  ws_bytes must be >= 4 * S_im2col. */
+spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const float *w_kcrs, float *y,
+                               int32_t fuse_relu, void *ws_lowered, size_t ws_bytes, void *stream);
+
+/* Host, synchronising (it times).  Per-layer offline selection:
+ * over the M sample maps (device, M*N*C*H*W fp32), time encode+conv for CPO
+ * and CPS and lowering+GEMM for im2col, `reps` times each, sum per algorithm
+ * and return the argmin under `mode` (ties prefer the sparse algorithm,
+ * reading A24).  times_ms (host float[3]) = {im2col, CPO, CPS} summed over
+ * the M samples, per rep.  Geometries the sparse path rejects choose im2col
+ * with times_ms[1..2] = -1.  ws: >= spc_select_ws_bytes(d). */
+spc_status select_layer_algo(const spc_conv_desc *d, const float *samples, int32_t M, const float *w_kcrs,
+                             spc_mode mode, int32_t reps, spc_algo *choice, float *times_ms, void *ws,
+                             size_t ws_bytes, void *stream);
+size_t spc_select_ws_bytes(const spc_conv_desc *d);
+
+/* Host, synchronising: copy the device `lengths` of an encoding to
+ * out_host[3] = {ptr_len, da_len, in_len}; returns SPC_ECAPACITY if the
+ * encoder reported an overflow. */
+spc_status spc_encoding_lengths(const spc_encoding *enc, int64_t out_host[3], void *stream);
+
+/* Thread-local message describing the last non-OK status of this thread. */
+const char *spc_last_error(void);
+
+/* Library build identification (sm_100a code object, git revision if known). */
+const char *spc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCONV_H */

@@ -72,6 +72,7 @@ def _L():
         sig = {
             "oc_out_h": (i32, [P]), "oc_out_w": (i32, [P]),
             "oc_direct_conv": (None, [P, vp, vp, vp]),
+            "oc_direct_conv_at": (None, [P, vp, vp, vp, i64, vp]),
             "oc_im2col": (i64, [P, vp, vp]),
             "oc_gemm_lowered": (None, [P, vp, vp, vp]),
             "oc_mec_lower": (i64, [P, vp, vp]),
@@ -115,6 +116,15 @@ def direct_conv(d: dict, x: np.ndarray, w: np.ndarray) -> np.ndarray:
     y = np.empty((d["N"], d["K"], Oh, Ow), dtype=np.float64)
     _L().oc_direct_conv(ctypes.byref(_desc(d)), _p(x), _p(w), _p(y))
     return y
+
+
+def direct_conv_at(d: dict, x: np.ndarray, w: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """Eq. 1 at output coordinates idx[i] = (n, k, y, x), FP64."""
+    idx = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1, 4)
+    x, w = _f32(x), _f32(w)
+    out = np.empty(idx.shape[0], dtype=np.float64)
+    _L().oc_direct_conv_at(ctypes.byref(_desc(d)), _p(x), _p(w), _p(idx), idx.shape[0], _p(out))
+    return out
 
 
 def im2col(d: dict, x: np.ndarray) -> np.ndarray:

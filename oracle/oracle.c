@@ -79,6 +79,25 @@ void oc_direct_conv(const oc_desc *d, const float *x, const float *w, double *y)
                 }
 }
 
+/* Eq. 1 at a list of output coordinates idx[i] = {n, k, y, x} (for parity at
+ * full size, where the whole output would take the oracle too long). */
+void oc_direct_conv_at(const oc_desc *d, const float *x, const float *w, const int32_t *idx, int64_t count,
+                       double *out)
+{
+    for (int64_t i = 0; i < count; i++) {
+        int32_t n = idx[4 * i], k = idx[4 * i + 1], oy = idx[4 * i + 2], ox = idx[4 * i + 3];
+        double acc = 0.0;
+        for (int32_t c = 0; c < d->C; c++) {
+            const float *pl = plane_of(x, d, n, c);
+            for (int32_t h = 0; h < d->R; h++)
+                for (int32_t ww = 0; ww < d->S; ww++)
+                    acc += (double)I_at(pl, d, oy * d->sh + h, ox * d->sw + ww) *
+                           (double)w[(((size_t)k * d->C + c) * d->R + h) * d->S + ww];
+        }
+        out[i] = acc;
+    }
+}
+
 /* ---------------------------------------------- im2col lowering */
 
 /* im2col: each kernel-sized patch of every channel becomes one row of the

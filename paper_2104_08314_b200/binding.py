@@ -1,0 +1,222 @@
+"""Thin ctypes binding of libspconv.so (include/spconv.h): argument marshalling only.
+
+Every function has the C name and calls straight into the library; tensors are
+torch CUDA tensors (device memory from PyTorch's allocator), the stream is
+torch's current stream unless given.  There is no CPU fallback: importing this
+module raises if the compiled sm_100a library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspconv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2104_08314_b200.build` "
+                      "(nvcc, sm_100a); there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+SPC_OK, SPC_EINVAL, SPC_EUNSUPPORTED, SPC_ECAPACITY, SPC_ECUDA, SPC_ECORRUPT = 0, -1, -2, -3, -4, -5
+SPC_ALGO_IM2COL, SPC_ALGO_CPO, SPC_ALGO_CPS = 0, 1, 2
+SPC_FAVOUR_TIME, SPC_FAVOUR_SPACE, SPC_BEST_OF_THREE = 0, 1, 2
+SPC_NPC = -(2 ** 31)
+SPC_NPF = -(2 ** 31) + 1
+ALGO_NAMES = {0: "im2col", 1: "cpo", 2: "cps"}
+
+
+class SpcError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.spc_last_error().decode()
+        super().__init__(f"{where} failed with status {status}: {msg}")
+        self.status = status
+
+
+class spc_conv_desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("N", "C", "H", "W", "K", "R", "S", "stride_h", "stride_w",
+                 "pad_top", "pad_bottom", "pad_left", "pad_right")]
+
+
+class spc_encoding(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("ptr_cap", ctypes.c_int64),
+                ("da", ctypes.c_void_p), ("da_cap", ctypes.c_int64),
+                ("in_", ctypes.c_void_p), ("in_cap", ctypes.c_int64),
+                ("chan_ptr_off", ctypes.c_void_p), ("chan_nz_off", ctypes.c_void_p),
+                ("chan_in_off", ctypes.c_void_p), ("lengths", ctypes.c_void_p),
+                ("algo", ctypes.c_int32), ("geom", spc_conv_desc)]
+
+
+_D = ctypes.POINTER(spc_conv_desc)
+_E = ctypes.POINTER(spc_encoding)
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_sigs = {
+    "spc_encode_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                            ctypes.POINTER(_sz)],
+    "spc_workspace_init": [_vp, _sz, _vp],
+    "cpo_encode": [_D, _vp, _E, _vp, _sz, _vp],
+    "cps_encode": [_D, _vp, _E, _vp, _sz, _vp],
+    "spc_pack_weights": [_D, _vp, _vp, _vp],
+    "sparse_conv_forward": [_D, _E, _vp, _vp, _i32, _vp, _sz, _vp],
+    "im2col_conv_forward": [_D, _vp, _vp, _vp, _i32, _vp, _sz, _vp],
+    "select_layer_algo": [_D, _vp, _i32, _vp, _i32, _i32, ctypes.POINTER(_i32),
+                          ctypes.POINTER(ctypes.c_float), _vp, _sz, _vp],
+    "spc_encoding_lengths": [_E, ctypes.POINTER(_i64), _vp],
+}
+for _n, _a in _sigs.items():
+    getattr(_lib, _n).argtypes = _a
+    getattr(_lib, _n).restype = ctypes.c_int
+_lib.spc_select_ws_bytes.argtypes = [_D]
+_lib.spc_select_ws_bytes.restype = _sz
+_lib.spc_last_error.restype = ctypes.c_char_p
+_lib.spc_version.restype = ctypes.c_char_p
+
+EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version"]
+
+
+def _check(rc: int, where: str):
+    if rc != SPC_OK:
+        raise SpcError(rc, where)
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_cuda:
+        raise ValueError("tensors passed to libspconv must be CUDA tensors")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def make_desc(d: dict) -> spc_conv_desc:
+    return spc_conv_desc(*(int(d[k]) for k in ("N", "C", "H", "W", "K", "R", "S", "stride_h", "stride_w",
+                                               "pad_top", "pad_bottom", "pad_left", "pad_right")))
+
+
+def out_hw(d: dict) -> tuple[int, int]:
+    """Output extents the library uses (include/spconv.h conventions)."""
+    Oh = (d["H"] + d["pad_top"] + d["pad_bottom"] - d["R"]) // d["stride_h"] + 1
+    Ow = (d["W"] + d["pad_left"] + d["pad_right"] - d["S"]) // d["stride_w"] + 1
+    return Oh, Ow
+
+
+def spc_encode_capacity(d: dict) -> tuple[int, int, int, int]:
+    p, a, i, w = _i64(), _i64(), _i64(), _sz()
+    _check(_lib.spc_encode_capacity(ctypes.byref(make_desc(d)), ctypes.byref(p), ctypes.byref(a),
+                                    ctypes.byref(i), ctypes.byref(w)), "spc_encode_capacity")
+    return p.value, a.value, i.value, w.value
+
+
+def spc_workspace_init(ws: torch.Tensor, stream=None):
+    _check(_lib.spc_workspace_init(_ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "spc_workspace_init")
+
+
+@dataclass
+class Encoding:
+    """Device buffers of one encoding (owned by PyTorch) + the C struct view."""
+    ptr: torch.Tensor
+    da: torch.Tensor
+    inn: torch.Tensor
+    chan_ptr_off: torch.Tensor
+    chan_nz_off: torch.Tensor
+    chan_in_off: torch.Tensor
+    lengths: torch.Tensor
+    c: spc_encoding = field(default_factory=spc_encoding)
+
+    def __post_init__(self):
+        self.c.ptr, self.c.ptr_cap = self.ptr.data_ptr(), self.ptr.numel()
+        self.c.da, self.c.da_cap = self.da.data_ptr(), self.da.numel()
+        self.c.in_, self.c.in_cap = self.inn.data_ptr(), self.inn.numel()
+        self.c.chan_ptr_off = self.chan_ptr_off.data_ptr()
+        self.c.chan_nz_off = self.chan_nz_off.data_ptr()
+        self.c.chan_in_off = self.chan_in_off.data_ptr()
+        self.c.lengths = self.lengths.data_ptr()
+
+    @property
+    def algo(self) -> int:
+        return self.c.algo
+
+
+def alloc_encoding(d: dict, device="cuda", caps: tuple[int, int, int] | None = None) -> Encoding:
+    pc, dc, ic, _ = spc_encode_capacity(d)
+    if caps is not None:
+        pc, dc, ic = caps
+    nc1 = d["N"] * d["C"] + 1
+    return Encoding(
+        ptr=torch.empty(max(pc, 1), dtype=torch.int32, device=device),
+        da=torch.empty(max(dc, 1), dtype=torch.float32, device=device),
+        inn=torch.empty(max(ic, 1), dtype=torch.int32, device=device),
+        chan_ptr_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        chan_nz_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        chan_in_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        lengths=torch.zeros(4, dtype=torch.int64, device=device))
+
+
+def alloc_workspace(d: dict, device="cuda") -> torch.Tensor:
+    """Encoder / CPS workspace, zeroed once (spc_workspace_init)."""
+    ws = torch.empty(spc_encode_capacity(d)[3], dtype=torch.uint8, device=device)
+    spc_workspace_init(ws)
+    return ws
+
+
+def cpo_encode(d: dict, x: torch.Tensor, enc: Encoding, ws: torch.Tensor, stream=None):
+    _check(_lib.cpo_encode(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _ptr(ws), ws.numel(),
+                           _stream(stream)), "cpo_encode")
+
+
+def cps_encode(d: dict, x: torch.Tensor, enc: Encoding, ws: torch.Tensor, stream=None):
+    _check(_lib.cps_encode(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _ptr(ws), ws.numel(),
+                           _stream(stream)), "cps_encode")
+
+
+def spc_pack_weights(d: dict, w: torch.Tensor, w_packed: torch.Tensor, stream=None):
+    _check(_lib.spc_pack_weights(ctypes.byref(make_desc(d)), _ptr(w), _ptr(w_packed), _stream(stream)),
+           "spc_pack_weights")
+
+
+def sparse_conv_forward(d: dict, enc: Encoding, w_packed: torch.Tensor, y: torch.Tensor, fuse_relu: bool = False,
+                        ws: torch.Tensor | None = None, stream=None):
+    _check(_lib.sparse_conv_forward(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(w_packed), _ptr(y),
+                                    int(fuse_relu), _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)),
+           "sparse_conv_forward")
+
+
+def im2col_conv_forward(d: dict, x: torch.Tensor, w: torch.Tensor, y: torch.Tensor, fuse_relu: bool,
+                        ws_lowered: torch.Tensor, stream=None):
+    _check(_lib.im2col_conv_forward(ctypes.byref(make_desc(d)), _ptr(x), _ptr(w), _ptr(y), int(fuse_relu),
+                                    _ptr(ws_lowered), ws_lowered.numel() * ws_lowered.element_size(),
+                                    _stream(stream)), "im2col_conv_forward")
+
+
+def spc_select_ws_bytes(d: dict) -> int:
+    return int(_lib.spc_select_ws_bytes(ctypes.byref(make_desc(d))))
+
+
+def select_layer_algo(d: dict, samples: torch.Tensor, M: int, w: torch.Tensor, mode: int, reps: int,
+                      ws: torch.Tensor, stream=None) -> tuple[int, list[float]]:
+    choice = _i32()
+    times = (ctypes.c_float * 3)()
+    _check(_lib.select_layer_algo(ctypes.byref(make_desc(d)), _ptr(samples), M, _ptr(w), mode, reps,
+                                  ctypes.byref(choice), times, _ptr(ws), ws.numel(), _stream(stream)),
+           "select_layer_algo")
+    return choice.value, [times[0], times[1], times[2]]
+
+
+def spc_encoding_lengths(enc: Encoding, stream=None) -> tuple[int, int, int]:
+    out = (_i64 * 3)()
+    _check(_lib.spc_encoding_lengths(ctypes.byref(enc.c), out, _stream(stream)), "spc_encoding_lengths")
+    return out[0], out[1], out[2]
+
+
+def spc_version() -> str:
+    return _lib.spc_version().decode()

@@ -1,0 +1,303 @@
+// api.cu -- extern "C" entry points of libspconv.so (declared in include/spconv.h).
+// Host-side validation, workspace carving, launches and the offline selector.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace spc {
+size_t enc_smem_bytes(const Geom& g);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+spc_status fail(spc_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+spc_status fail(spc_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+spc_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return SPC_OK;
+    return fail(SPC_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+spc_status check_desc(const spc_conv_desc* d) {
+    if (!d) return fail(SPC_EINVAL, "null descriptor");
+    if (d->N < 1 || d->C < 1 || d->H < 1 || d->W < 1 || d->K < 1 || d->R < 1 || d->S < 1)
+        return fail(SPC_EINVAL, "dimensions must be >= 1");
+    if (d->stride_h < 1 || d->stride_w < 1) return fail(SPC_EINVAL, "strides must be >= 1");
+    if (d->pad_top < 0 || d->pad_bottom < 0 || d->pad_left < 0 || d->pad_right < 0)
+        return fail(SPC_EINVAL, "negative padding");
+    if (d->H + d->pad_top + d->pad_bottom < d->R || d->W + d->pad_left + d->pad_right < d->S)
+        return fail(SPC_EINVAL, "kernel larger than the padded input");
+    return SPC_OK;
+}
+
+// Preconditions of the canonical encoding (DESIGN.md A.1).
+spc_status check_sparse_geometry(const spc_conv_desc* d) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    const int Wp = d->W + d->pad_left + d->pad_right;
+    if (d->R == 1 && d->S == 1) return fail(SPC_EUNSUPPORTED, "pointwise kernels are routed to im2col (PAPER.md:123)");
+    if (d->S > 8) return fail(SPC_EUNSUPPORTED, "K_w > 8 not supported");
+    if (d->S > 1) {
+        if (d->pad_left != d->pad_right) return fail(SPC_EUNSUPPORTED, "pad_left != pad_right (reading A16)");
+        if (d->pad_left > d->S - 1) return fail(SPC_EUNSUPPORTED, "pad_left >= K_w");
+        if (Wp < 2 * d->S - 1) return fail(SPC_EUNSUPPORTED, "padded width < 2*K_w - 1 (reading A17)");
+    } else if (d->pad_left || d->pad_right) {
+        return fail(SPC_EUNSUPPORTED, "K_w = 1 with horizontal padding");
+    }
+    if (d->pad_top > d->R - 1 || d->pad_bottom > d->R - 1) return fail(SPC_EUNSUPPORTED, "vertical pad >= K_h");
+    if ((long long)d->H * d->W * 4 > spc::kEncMaxPlaneBytes)
+        return fail(SPC_EUNSUPPORTED, "channel plane larger than the encoder smem stage");
+    const long long Hp = d->H + d->pad_top + d->pad_bottom;
+    if ((long long)(d->S - 1) + (Hp - 1) * d->S >= (1ll << 31)) return fail(SPC_EUNSUPPORTED, "index overflow");
+    return SPC_OK;
+}
+
+void caps_of(const spc::Geom& g, int64_t* pc, int64_t* dc, int64_t* ic) {
+    const long long per = (g.S == 1) ? (1 + g.Ow1) : (3 + (long long)(g.S - 1) * (1 + g.Ow1));
+    *pc = g.NC * per;
+    *dc = g.NC * g.H * g.W;
+    *ic = *dc;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+spc_status do_encode(const spc_conv_desc* d, const float* x, spc_encoding* out, void* ws, size_t ws_bytes,
+                     void* stream, bool cps) {
+    spc_status s = check_sparse_geometry(d);
+    if (s != SPC_OK) return s;
+    if (!x || !out || !ws) return fail(SPC_EINVAL, "null pointer");
+    if (!out->ptr || !out->da || !out->in || !out->chan_ptr_off || !out->chan_nz_off || !out->chan_in_off ||
+        !out->lengths)
+        return fail(SPC_EINVAL, "null stream pointer in spc_encoding");
+    if (!aligned16(x)) return fail(SPC_EINVAL, "x must be 16-byte aligned");
+    spc::Geom g = spc::make_geom(*d);
+    if ((size_t)spc::ws_layout(g).cps_in > ws_bytes) return fail(SPC_EINVAL, "workspace too small");
+    if (out->ptr_cap < 0 || out->da_cap < 0 || out->in_cap < 0) return fail(SPC_EINVAL, "negative capacity");
+    out->algo = (cps && d->S > 1) ? SPC_ALGO_CPS : (cps ? SPC_ALGO_CPS : SPC_ALGO_CPO);
+    out->geom = *d;
+    return cuda_status(spc::launch_encode(g, cps && d->S > 1, x, out, ws, (cudaStream_t)stream), "encode");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spc_last_error(void) { return g_err.c_str(); }
+
+const char* spc_version(void) {
+#ifndef SPC_GIT_REV
+#define SPC_GIT_REV "unknown"
+#endif
+    return "spconv-b200 sm_100a rev " SPC_GIT_REV;
+}
+
+spc_status spc_encode_capacity(const spc_conv_desc* d, int64_t* ptr_cap, int64_t* da_cap, int64_t* in_cap,
+                               size_t* ws_bytes) {
+    spc_status s = check_sparse_geometry(d);
+    if (s != SPC_OK) return s;
+    spc::Geom g = spc::make_geom(*d);
+    int64_t pc, dc, ic;
+    caps_of(g, &pc, &dc, &ic);
+    if (ptr_cap) *ptr_cap = pc;
+    if (da_cap) *da_cap = dc;
+    if (in_cap) *in_cap = ic;
+    if (ws_bytes) *ws_bytes = spc::ws_layout(g).total;
+    return SPC_OK;
+}
+
+spc_status spc_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+    if (!ws) return fail(SPC_EINVAL, "null workspace");
+    cudaError_t e = cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    return cuda_status(e, "spc_workspace_init");
+}
+
+spc_status cpo_encode(const spc_conv_desc* d, const float* x, spc_encoding* out, void* ws, size_t ws_bytes,
+                      void* stream) {
+    return do_encode(d, x, out, ws, ws_bytes, stream, false);
+}
+
+spc_status cps_encode(const spc_conv_desc* d, const float* x, spc_encoding* out, void* ws, size_t ws_bytes,
+                      void* stream) {
+    return do_encode(d, x, out, ws, ws_bytes, stream, true);
+}
+
+spc_status spc_pack_weights(const spc_conv_desc* d, const float* w_kcrs, float* w_packed, void* stream) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!w_kcrs || !w_packed) return fail(SPC_EINVAL, "null pointer");
+    spc::Geom g = spc::make_geom(*d);
+    return cuda_status(spc::launch_pack_weights(g, w_kcrs, w_packed, (cudaStream_t)stream), "pack_weights");
+}
+
+spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed, float* y,
+                               int32_t fuse_relu, void* ws, size_t ws_bytes, void* stream) {
+    spc_status s = check_sparse_geometry(d);
+    if (s != SPC_OK) return s;
+    if (!enc || !w_packed || !y) return fail(SPC_EINVAL, "null pointer");
+    const spc_conv_desc& e = enc->geom;
+    if (e.N != d->N || e.C != d->C || e.H != d->H || e.W != d->W || e.R != d->R || e.S != d->S ||
+        e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom || e.pad_left != d->pad_left ||
+        e.pad_right != d->pad_right)
+        return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
+    spc::Geom g = spc::make_geom(*d);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int32_t* in_cpo = nullptr;
+    if (enc->algo == SPC_ALGO_CPS && d->S > 1) {
+        spc::WsLayout L = spc::ws_layout(g);
+        if (!ws || ws_bytes < L.total) return fail(SPC_EINVAL, "CPS convolution needs the workspace");
+        int32_t* buf = reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.cps_in);
+        spc_status r = cuda_status(spc::launch_cps_expand(g, enc, buf, st), "cps_expand");
+        if (r != SPC_OK) return r;
+        in_cpo = buf;
+    }
+    return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, st), "sparse_conv");
+}
+
+spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const float* w_kcrs, float* y,
+                               int32_t fuse_relu, void* ws_lowered, size_t ws_bytes, void* stream) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!x || !w_kcrs || !y || !ws_lowered) return fail(SPC_EINVAL, "null pointer");
+    spc::Geom g = spc::make_geom(*d);
+    const size_t need = (size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow;
+    if (ws_bytes < need) return fail(SPC_EINVAL, "lowered-matrix workspace too small (%zu < %zu)", ws_bytes, need);
+    cudaStream_t st = (cudaStream_t)stream;
+    float* L = static_cast<float*>(ws_lowered);
+    spc_status r = cuda_status(spc::launch_im2col(g, x, L, st), "im2col");
+    if (r != SPC_OK) return r;
+    return cuda_status(spc::launch_gemm(g, w_kcrs, L, y, fuse_relu, st), "gemm");
+}
+
+spc_status spc_encoding_lengths(const spc_encoding* enc, int64_t out_host[3], void* stream) {
+    if (!enc || !enc->lengths || !out_host) return fail(SPC_EINVAL, "null pointer");
+    int64_t h[4];
+    cudaError_t e = cudaMemcpyAsync(h, enc->lengths, sizeof h, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "spc_encoding_lengths");
+    out_host[0] = h[0]; out_host[1] = h[1]; out_host[2] = h[2];
+    if (h[3]) return fail(SPC_ECAPACITY, "encoder overflow: needs ptr %lld da %lld in %lld", (long long)h[0],
+                          (long long)h[1], (long long)h[2]);
+    return SPC_OK;
+}
+
+// ------------------------------------------------------------ selection
+
+size_t spc_select_ws_bytes(const spc_conv_desc* d) {
+    if (check_desc(d) != SPC_OK) return 0;
+    spc::Geom g = spc::make_geom(*d);
+    size_t total = 0;
+    const size_t lowered = spc::align_up((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow, 256);
+    const size_t yb = spc::align_up((size_t)4 * g.N * g.K * g.Oh * g.Ow, 256);
+    const size_t wpb = spc::align_up((size_t)4 * g.K * g.C * g.R * g.S, 256);
+    total += lowered + yb + wpb;
+    if (check_sparse_geometry(d) == SPC_OK) {
+        int64_t pc, dc, ic;
+        caps_of(g, &pc, &dc, &ic);
+        total += spc::align_up(4 * pc, 256) + spc::align_up(4 * dc, 256) + spc::align_up(4 * ic, 256);
+        total += 3 * spc::align_up(8 * (g.NC + 1), 256) + 256;
+        total += spc::ws_layout(g).total;
+    }
+    g_err.clear();
+    return total;
+}
+
+spc_status select_layer_algo(const spc_conv_desc* d, const float* samples, int32_t M, const float* w_kcrs,
+                             spc_mode mode, int32_t reps, spc_algo* choice, float* times_ms, void* ws,
+                             size_t ws_bytes, void* stream) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!samples || !w_kcrs || !choice || !times_ms || !ws || M < 1 || reps < 1)
+        return fail(SPC_EINVAL, "bad argument");
+    if (ws_bytes < spc_select_ws_bytes(d)) return fail(SPC_EINVAL, "selection workspace too small");
+    spc::Geom g = spc::make_geom(*d);
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned char* p = static_cast<unsigned char*>(ws);
+    auto take = [&](size_t b) { unsigned char* r = p; p += spc::align_up(b, 256); return r; };
+    float* lowered = reinterpret_cast<float*>(take((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow));
+    float* y = reinterpret_cast<float*>(take((size_t)4 * g.N * g.K * g.Oh * g.Ow));
+    float* wp = reinterpret_cast<float*>(take((size_t)4 * g.K * g.C * g.R * g.S));
+    const bool sparse_ok = check_sparse_geometry(d) == SPC_OK;
+    g_err.clear();
+    const size_t per_sample = (size_t)g.N * g.C * g.H * g.W;
+    const size_t lowered_bytes = (size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow;
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+        return fail(SPC_ECUDA, "event create");
+    float t[3] = {0.f, -1.f, -1.f};
+    spc_status r = SPC_OK;
+    // im2col: lowering + GEMM
+    for (int rep = 0; rep < reps + 1 && r == SPC_OK; rep++) {
+        cudaEventRecord(e0, st);
+        for (int m = 0; m < M && r == SPC_OK; m++)
+            r = im2col_conv_forward(d, samples + m * per_sample, w_kcrs, y, 0, lowered, lowered_bytes, stream);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0) t[0] += ms;  // rep 0 is warm-up
+    }
+    if (sparse_ok && r == SPC_OK) {
+        spc_encoding enc;
+        memset(&enc, 0, sizeof enc);
+        int64_t pc, dc, ic;
+        caps_of(g, &pc, &dc, &ic);
+        enc.ptr = reinterpret_cast<int32_t*>(take(4 * pc)); enc.ptr_cap = pc;
+        enc.da = reinterpret_cast<float*>(take(4 * dc)); enc.da_cap = dc;
+        enc.in = reinterpret_cast<int32_t*>(take(4 * ic)); enc.in_cap = ic;
+        enc.chan_ptr_off = reinterpret_cast<int64_t*>(take(8 * (g.NC + 1)));
+        enc.chan_nz_off = reinterpret_cast<int64_t*>(take(8 * (g.NC + 1)));
+        enc.chan_in_off = reinterpret_cast<int64_t*>(take(8 * (g.NC + 1)));
+        enc.lengths = reinterpret_cast<int64_t*>(take(64));
+        const size_t ews = spc::ws_layout(g).total;
+        void* ew = take(ews);
+        r = cuda_status(cudaMemsetAsync(ew, 0, ews, st), "select ws init");
+        if (r == SPC_OK) r = spc_pack_weights(d, w_kcrs, wp, stream);
+        for (int a = 0; a < 2 && r == SPC_OK; a++) {
+            const bool cps = a == 1;
+            float tot = 0.f;
+            for (int rep = 0; rep < reps + 1 && r == SPC_OK; rep++) {
+                cudaEventRecord(e0, st);
+                for (int m = 0; m < M && r == SPC_OK; m++) {
+                    r = cps ? cps_encode(d, samples + m * per_sample, &enc, ew, ews, stream)
+                            : cpo_encode(d, samples + m * per_sample, &enc, ew, ews, stream);
+                    if (r == SPC_OK) r = sparse_conv_forward(d, &enc, wp, y, 0, ew, ews, stream);
+                }
+                cudaEventRecord(e1, st);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (rep > 0) tot += ms;
+            }
+            t[1 + a] = tot;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (r != SPC_OK) return r;
+    for (int i = 0; i < 3; i++) times_ms[i] = (t[i] >= 0.f) ? t[i] / reps : -1.f;
+    // argmin; ties prefer the smaller footprint: CPS over CPO over im2col (reading A24)
+    spc_algo best = SPC_ALGO_IM2COL;
+    float tb = times_ms[0];
+    if (sparse_ok) {
+        if (mode != SPC_FAVOUR_SPACE && times_ms[1] <= tb) { best = SPC_ALGO_CPO; tb = times_ms[1]; }
+        if (mode != SPC_FAVOUR_TIME && times_ms[2] <= tb) { best = SPC_ALGO_CPS; tb = times_ms[2]; }
+    }
+    *choice = best;
+    return SPC_OK;
+}
+
+}  // extern "C"

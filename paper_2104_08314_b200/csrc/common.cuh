@@ -1,0 +1,119 @@
+// common.cuh -- internal helpers of the sm_100a CPO/CPS library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spconv.h"
+
+namespace spc {
+
+constexpr int kWarp = 32;
+
+// Geometry shared by encoder and convolution kernels (host-computed).
+struct Geom {
+    int N, C, H, W, K, R, S, sh, sw, pt, pb, pl, pr;
+    int Hp, Wp;      // padded extents
+    int Ow1, Oh1;    // stride-1 partition / output counts
+    int Oh, Ow;      // output extents at the real stride (floor, reading A14)
+    int nwords;      // 32-bit words per padded column mask = ceil(Hp / 32)
+    long long NC;    // N * C channel planes
+};
+
+inline Geom make_geom(const spc_conv_desc& d) {
+    Geom g;
+    g.N = d.N; g.C = d.C; g.H = d.H; g.W = d.W; g.K = d.K; g.R = d.R; g.S = d.S;
+    g.sh = d.stride_h; g.sw = d.stride_w;
+    g.pt = d.pad_top; g.pb = d.pad_bottom; g.pl = d.pad_left; g.pr = d.pad_right;
+    g.Hp = d.H + d.pad_top + d.pad_bottom;
+    g.Wp = d.W + d.pad_left + d.pad_right;
+    g.Ow1 = g.Wp - d.S + 1;
+    g.Oh1 = g.Hp - d.R + 1;
+    g.Oh = (g.Hp - d.R) / d.stride_h + 1;
+    g.Ow = (g.Wp - d.S) / d.stride_w + 1;
+    g.nwords = (g.Hp + 31) / 32;
+    g.NC = (long long)d.N * d.C;
+    return g;
+}
+
+// Encoder: four channel planes per CTA (one per warp).
+constexpr int kEncWarps = 4;
+constexpr int kEncMaxPlaneBytes = 200 * 1024 / kEncWarps;  // smem stage per plane
+
+// Decoupled look-back state of the single-pass encoder (lives in the workspace).
+struct EncState {
+    int ticket;   // dynamic tile counter (CTA start order)
+    int done;     // finished CTAs (the last one resets the state)
+    int pad[2];
+};
+
+__host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+inline long long enc_tiles(const Geom& g) { return (g.NC + kEncWarps - 1) / kEncWarps; }
+
+// Workspace layout: [EncState | flags[ntiles] | agg[3*ntiles] | inc[3*ntiles] | cps_in[da_cap]]
+struct WsLayout {
+    size_t state, flags, agg, inc, cps_in, total;
+};
+
+inline WsLayout ws_layout(const Geom& g) {
+    WsLayout L;
+    long long nt = enc_tiles(g);
+    L.state = 0;
+    L.flags = align_up(sizeof(EncState), 256);
+    L.agg = align_up(L.flags + sizeof(int) * (size_t)nt, 256);
+    L.inc = align_up(L.agg + sizeof(long long) * 3 * (size_t)nt, 256);
+    L.cps_in = align_up(L.inc + sizeof(long long) * 3 * (size_t)nt, 256);
+    L.total = align_up(L.cps_in + sizeof(int32_t) * (size_t)(g.NC * g.H * g.W), 256);
+    return L;
+}
+
+// ---- device helpers --------------------------------------------------------
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_exclusive_scan(T v, T* total) {
+    const int lane = threadIdx.x & 31;
+    T inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    *total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - v;
+}
+
+}  // namespace spc
+
+// Internal launchers (defined in the .cu files, called from api.cu).
+namespace spc {
+cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding* e, void* ws, cudaStream_t st);
+cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaStream_t st);
+cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st);
+cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
+                               const float* w_packed, float* y, int relu, cudaStream_t st);
+cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
+cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
+}  // namespace spc

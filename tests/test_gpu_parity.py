@@ -1,0 +1,238 @@
+"""CUDA path vs the CPU oracle, element by element, through the C ABI.
+
+Encodings (ptr, DA bits, IN, side tables, lengths) must be bit-exact; conv
+outputs within |gpu - ref| <= max(1e-4 |ref|, 1e-5) of the FP64 oracle
+(BASELINE.json north_star), and exactly equal on integer-valued data.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from gpu_util import GpuLayer, assert_streams_equal  # noqa: E402
+from helpers import within_tol, valid_sparse_geometry  # noqa: E402
+from synth import (CONFIGS, cfg5_layers, clustered_relu, he_normal, int_map, int_weights,  # noqa: E402
+                   layer_desc)
+
+import paper_2104_08314_b200 as spc  # noqa: E402
+
+KERNELS = [(3, 3, 1), (3, 3, 2), (1, 7, 1), (7, 1, 1), (4, 4, 1), (5, 5, 1), (3, 1, 1), (1, 3, 2), (2, 2, 1),
+           (3, 5, 2)]
+
+
+def _cases(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        R, S, s = KERNELS[rng.integers(len(KERNELS))]
+        pl = int(rng.integers(0, S)) if S > 1 else 0
+        pt, pb = (int(rng.integers(0, R)) for _ in range(2))
+        H = int(rng.integers(max(1, R - pt - pb), 20))
+        W = int(rng.integers(max(1, 2 * S - 1 - 2 * pl), 20))
+        d = layer_desc(int(rng.integers(1, 4)), int(rng.integers(1, 9)), H, W,
+                       int(rng.choice([1, 5, 32, 40, 70])), R, S, s, s, pt, pb, pl, pl)
+        if not valid_sparse_geometry(d):
+            continue
+        out.append((d, float(rng.choice([0.0, 0.05, 0.3, 0.6, 1.0])), int(rng.integers(1 << 30))))
+    return out
+
+
+SWEEP = _cases(80, 7)
+
+
+@pytest.mark.parametrize("i", range(len(SWEEP)))
+def test_sweep_integer_exact(oracle_mod, i):
+    d, rho, seed = SWEEP[i]
+    x = int_map(d["N"], d["C"], d["H"], d["W"], rho, seed)
+    w = int_weights(d["K"], d["C"], d["R"], d["S"], seed)
+    ref = oracle_mod.direct_conv(d, x, w)
+    xg = torch.from_numpy(x).cuda()
+    L = GpuLayer(d, w)
+    for cps in (False, True):
+        L.encode(xg, cps)
+        assert_streams_equal(L.streams(), oracle_mod.encode(d, x, cps=cps), f"{d} cps={cps}")
+        got = L.conv().cpu().numpy()
+        assert np.array_equal(got, ref), f"{d} cps={cps} max err {np.abs(got - ref).max()}"
+    assert np.array_equal(L.im2col(xg).cpu().numpy(), ref)
+
+
+def _check_conv(got, ref, what):
+    ok, err, nbad = within_tol(got, ref)
+    assert ok, f"{what}: {nbad} elements out of tolerance, max abs err {err}"
+
+
+def _layer_case(oracle_mod, d, x, w, full=True, samples=4000, seed=0):
+    xg = torch.from_numpy(x).cuda()
+    L = GpuLayer(d, w)
+    outs = {}
+    for cps in (False, True):
+        L.encode(xg, cps)
+        assert_streams_equal(L.streams(), oracle_mod.encode(d, x, cps=cps), f"cps={cps}")
+        outs[cps] = L.conv().cpu().numpy()
+    outs["im2col"] = L.im2col(xg).cpu().numpy()
+    if full:
+        ref = oracle_mod.direct_conv(d, x, w)
+        for k, v in outs.items():
+            _check_conv(v, ref, f"algo {k}")
+    else:
+        rng = np.random.default_rng(seed)
+        shp = outs[False].shape
+        idx = np.stack([rng.integers(0, s, samples) for s in shp], axis=1)
+        ref = oracle_mod.direct_conv_at(d, x, w, idx)
+        for k, v in outs.items():
+            got = v[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]]
+            _check_conv(got, ref, f"algo {k} (sampled)")
+        # properties that hold everywhere: CPO == CPS closely, finite
+        assert np.isfinite(outs[False]).all()
+        _check_conv(outs[True], outs[False].astype(np.float64), "cps vs cpo")
+    return outs
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg3s2"])
+def test_baseline_configs_full(oracle_mod, name):
+    c = CONFIGS[name]
+    d = c["desc"]
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"], c["dead_frac"],
+                       c["zero_tile_frac"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    _layer_case(oracle_mod, d, x, w, full=True)
+
+
+@pytest.mark.parametrize("rho", [0.05, 0.2, 0.3, 0.5])
+def test_cfg3_density_sweep(oracle_mod, rho):
+    c = CONFIGS["cfg3"]
+    d = c["desc"]
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], rho, c["seed"], c["dead_frac"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    _layer_case(oracle_mod, d, x, w, full=False)
+
+
+def test_cfg4_pair_relu_chain(oracle_mod):
+    a, b = CONFIGS["cfg4a"], CONFIGS["cfg4b"]
+    da, db = a["desc"], b["desc"]
+    x = clustered_relu(da["N"], da["C"], da["H"], da["W"], a["density"], a["seed"], a["dead_frac"])
+    w1 = he_normal(da["K"], da["C"], da["R"], da["S"], a["seed"])
+    w2 = he_normal(db["K"], db["C"], db["R"], db["S"], a["seed"] + 1)
+    L1 = GpuLayer(da, w1)
+    L1.encode(torch.from_numpy(x).cuda())
+    assert_streams_equal(L1.streams(), oracle_mod.encode(da, x), "1x7")
+    y1 = L1.conv(relu=True).cpu().numpy()          # ReLU fused in the epilogue
+    ref1 = np.maximum(oracle_mod.direct_conv(da, x, w1), 0.0)
+    _check_conv(y1, ref1, "1x7 + relu")
+    # the 7x1 layer consumes the GPU intermediate; both sides encode the same tensor
+    rho = float((y1 != 0).mean())
+    assert 0.2 < rho < 0.8
+    _layer_case(oracle_mod, db, y1, w2, full=True)
+
+
+@pytest.mark.parametrize("li", [0, 3, 4, 8, 12, 15])
+def test_cfg5_layers_sampled(oracle_mod, li):
+    layer = cfg5_layers(batch=32)[li]
+    d = layer["desc"]
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], layer["density"], layer["seed"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], layer["seed"])
+    _layer_case(oracle_mod, d, x, w, full=False, samples=3000, seed=li)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def _desc3(**kw):
+    d = layer_desc(2, 6, 13, 11, 40, 3, 3, 1, 1, 1, 1, 1, 1)
+    d.update(kw)
+    return d
+
+
+def test_all_zero_input_is_all_npc(oracle_mod):
+    d = _desc3()
+    x = np.zeros((2, 6, 13, 11), dtype=np.float32)
+    L = GpuLayer(d, int_weights(40, 6, 3, 3, 1))
+    L.encode(torch.from_numpy(x).cuda())
+    s = L.streams()
+    assert (s["ptr"] == spc.SPC_NPC).all() and s["ptr"].size == 12 and s["da"].size == 0
+    assert not L.conv().any()
+
+
+def test_density_one_and_single_corners(oracle_mod):
+    d = _desc3(pad_top=0, pad_bottom=0, pad_left=0, pad_right=0)
+    w = int_weights(40, 6, 3, 3, 2)
+    for x in (np.ones((2, 6, 13, 11), np.float32),):
+        _layer_case(oracle_mod, d, x, w)
+    x = np.zeros((2, 6, 13, 11), np.float32)
+    x[0, 0, 0, 0] = 3; x[0, 1, 12, 10] = 5; x[1, 5, 0, 10] = -2; x[1, 2, 12, 0] = 7
+    _layer_case(oracle_mod, d, x, w)
+
+
+def test_negative_zero_and_denormals(oracle_mod):
+    """-0.0 is zero, a denormal is an NZE (IEEE != 0, reading A21)."""
+    d = _desc3()
+    x = np.zeros((2, 6, 13, 11), np.float32)
+    x[0, 0, 3, 3] = -0.0
+    x[0, 1, 4, 4] = np.float32(1e-40)
+    x[1, 2, 5, 5] = 1.0
+    L = GpuLayer(d, int_weights(40, 6, 3, 3, 2))
+    L.encode(torch.from_numpy(x).cuda())
+    ref = oracle_mod.encode(d, x)
+    assert ref["da"].size == 2
+    assert_streams_equal(L.streams(), ref)
+
+
+def test_relu_fusion_and_repeat(oracle_mod):
+    d = _desc3()
+    x = clustered_relu(2, 6, 13, 11, 0.4, 3)
+    w = he_normal(40, 6, 3, 3, 3)
+    L = GpuLayer(d, w)
+    xg = torch.from_numpy(x).cuda()
+    first = None
+    for _ in range(3):   # the encoder workspace must come back clean every launch
+        L.encode(xg)
+        s = L.streams()
+        if first is None:
+            first = s
+        assert_streams_equal(s, first)
+    y = L.conv(relu=True).cpu().numpy()
+    _check_conv(y, np.maximum(oracle_mod.direct_conv(d, x, w), 0), "relu")
+
+
+def test_capacity_overflow_reported(oracle_mod):
+    d = _desc3()
+    x = clustered_relu(2, 6, 13, 11, 0.5, 4)
+    L = GpuLayer(d, caps=(1000, 100, 100))
+    L.encode(torch.from_numpy(x).cuda())
+    with pytest.raises(spc.SpcError) as e:
+        spc.spc_encoding_lengths(L.enc)
+    assert e.value.status == spc.SPC_ECAPACITY
+
+
+def test_unsupported_geometry_raises():
+    L = GpuLayer(_desc3())
+    x = torch.zeros((2, 6, 13, 11), device="cuda")
+    with pytest.raises(spc.SpcError) as e:
+        spc.cpo_encode(_desc3(pad_left=1, pad_right=0), x, L.enc, L.ws)
+    assert e.value.status == spc.SPC_EUNSUPPORTED
+
+
+def test_select_layer_algo_argmin():
+    c = CONFIGS["cfg1"]
+    d = c["desc"]
+    M = 5
+    xs = np.stack([clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], s, c["dead_frac"])
+                   for s in c["select_seeds"]])
+    w = torch.from_numpy(he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])).cuda()
+    ws = torch.empty(spc.spc_select_ws_bytes(d), dtype=torch.uint8, device="cuda")
+    samples = torch.from_numpy(xs).cuda()
+    for mode, allowed in ((spc.SPC_FAVOUR_TIME, {0, 1}), (spc.SPC_FAVOUR_SPACE, {0, 2}),
+                          (spc.SPC_BEST_OF_THREE, {0, 1, 2})):
+        choice, t = spc.select_layer_algo(d, samples, M, w, mode, 3, ws)
+        assert choice in allowed and all(v > 0 for v in t)
+        cand = [a for a in allowed]
+        assert t[choice] <= min(t[a] for a in cand) + 1e-9
+    # pointwise -> im2col, sparse times reported as -1
+    dp = dict(d, R=1, S=1, pad_top=0, pad_bottom=0, pad_left=0, pad_right=0)
+    ws2 = torch.empty(spc.spc_select_ws_bytes(dp), dtype=torch.uint8, device="cuda")
+    wp = torch.from_numpy(he_normal(d["K"], d["C"], 1, 1, 1)).cuda()
+    choice, t = spc.select_layer_algo(dp, samples, M, wp, spc.SPC_BEST_OF_THREE, 2, ws2)
+    assert choice == spc.SPC_ALGO_IM2COL and t[1] == -1 and t[2] == -1

@@ -1,0 +1,55 @@
+// ffma_peak.cu -- measured FP32 FFMA throughput on this B200 (the roofline
+// denominator of the sparse conv, which runs on the FFMA pipe).
+// Two forms: 3-register FFMA (acc = a*b + acc, as in the conv's inner loop)
+// and register-reuse chains.  Prints TFLOP/s and the SM clock seen.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int ILP>
+__global__ void __launch_bounds__(256) ffma_kernel(float* out, float a, float b, int iters) {
+    float acc[ILP];
+    float w[ILP];
+#pragma unroll
+    for (int i = 0; i < ILP; i++) { acc[i] = threadIdx.x * 1e-3f + i; w[i] = b + i * 1e-4f; }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < ILP; i++) acc[i] = fmaf(a, w[i], acc[i]);
+#pragma unroll
+        for (int i = 0; i < ILP; i++) acc[i] = fmaf(w[i], a, acc[i]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < ILP; i++) s += acc[i];
+    if (s == 12345.678f) out[0] = s;
+}
+
+int main() {
+    float* out;
+    cudaMalloc(&out, 4);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int iters = 1 << 14;
+    dim3 grid(sms * 8), block(256);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int rep = 0; rep < 3; rep++) ffma_kernel<16><<<grid, block>>>(out, 1.0001f, 0.9999f, iters);
+    cudaDeviceSynchronize();
+    float best = 0.f;
+    for (int rep = 0; rep < 10; rep++) {
+        cudaEventRecord(e0);
+        ffma_kernel<16><<<grid, block>>>(out, 1.0001f, 0.9999f, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 2 * 16 * (double)iters * grid.x * block.x;
+        double tf = flops / (ms * 1e-3) / 1e12;
+        if (tf > best) best = tf;
+    }
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("{\"ffma_tflops_best\": %.2f, \"sms\": %d, \"max_clock_mhz\": %d, \"nominal_tflops\": %.2f}\n", best, sms,
+           clk / 1000, sms * 128 * 2 * (clk / 1000.0) * 1e6 / 1e12);
+    return 0;
+}
