@@ -76,46 +76,54 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled with NVML every ~1 ms during the timed region."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.maxclk = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def _sample(self):
+        clk = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.rows.append((clk, rs))
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                break
+            time.sleep(0.001)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
             try:
-                self.proc.wait(timeout=2)
+                self._sample()
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
-        if not self.rows:
+        if not self.rows or self.nv is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+        reasons = sorted({n for _, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.rows), "sm_max_mhz": self.maxclk,
                 "reasons": reasons, "samples": len(self.rows)}
 
 
@@ -190,62 +198,50 @@ def run_ours(args):
     x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"] + 7919 * rank, c["dead_frac"],
                        c["zero_tile_frac"])
     w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    from paper_2104_08314_b200.layer import SparseConvLayer
     Oh, Ow = spc.out_hw(d)
     xg = torch.from_numpy(x).to(dev)
     wg = torch.from_numpy(w).to(dev)
-    wp = torch.empty_like(wg).reshape(-1)
-    spc.spc_pack_weights(d, wg, wp)
-    enc = spc.alloc_encoding(d, device=dev)
-    enc_s = spc.alloc_encoding(d, device=dev)
-    ws = spc.alloc_workspace(d, device=dev)
-    y = torch.empty((d["N"], d["K"], Oh, Ow), device=dev)
-    lowered = torch.empty(d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow, device=dev)
+    L_cpo = SparseConvLayer(d, wg, device=dev)
+    L_cps = SparseConvLayer(d, wg, device=dev)
+    y = L_cpo.y
+    enc, enc_s = L_cpo.enc, L_cps.enc
     flush = torch.empty(int(2 * 128 * 2 ** 20) // 4, dtype=torch.float32, device=dev)  # > 2x L2
 
-    def step_cpo(e0=None, e1=None, e2=None):
-        if e0 is not None: e0.record(stream)
-        spc.cpo_encode(d, xg, enc, ws)
-        if e1 is not None: e1.record(stream)
-        spc.sparse_conv_forward(d, enc, wp, y, False, ws)
-        if e2 is not None: e2.record(stream)
+    # CUDA graphs of each step: the host enqueues a whole step at once, so the
+    # device timeline between the events holds only our kernels.
+    g_cpo = L_cpo.capture(lambda: L_cpo.forward(xg, "cpo"))
+    g_cpo_enc = L_cpo.capture(lambda: L_cpo.encode(xg, "cpo"))
+    g_cpo_conv = L_cpo.capture(lambda: L_cpo.conv())
+    g_cps = L_cps.capture(lambda: L_cps.forward(xg, "cps"))
+    g_cps_enc = L_cps.capture(lambda: L_cps.encode(xg, "cps"))
+    g_i2c = L_cpo.capture(lambda: L_cpo.forward(xg, "im2col"))
+    L_cpo.forward(xg, "cpo")       # leave the CPO encoding in place for the conv-only graph
 
-    def step_cps(e0=None, e1=None, e2=None):
-        if e0 is not None: e0.record(stream)
-        spc.cps_encode(d, xg, enc_s, ws)
-        if e1 is not None: e1.record(stream)
-        spc.sparse_conv_forward(d, enc_s, wp, y, False, ws)
-        if e2 is not None: e2.record(stream)
-
-    def step_im2col(e0=None, e1=None, e2=None):
-        if e0 is not None: e0.record(stream)
-        spc.im2col_conv_forward(d, xg, wg, y, False, lowered)
-        if e2 is not None: e2.record(stream)
-
-    def timed(fn, steps, warmup, split=True):
+    def timed(graph, steps, warmup):
         for _ in range(warmup):
-            fn()
+            graph.replay()
         torch.cuda.synchronize()
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         for i in range(steps):
             flush.zero_()                      # L2 flush between timed steps (outside the events)
-            fn(*ev[i])
+            ev[i][0].record(stream)
+            graph.replay()
+            ev[i][1].record(stream)
         torch.cuda.synchronize()
-        tot = [e[0].elapsed_time(e[2]) for e in ev]
-        first = [e[0].elapsed_time(e[1]) for e in ev] if split else [0.0] * steps
-        return sum(tot), sum(first)
+        return sum(a.elapsed_time(b) for a, b in ev)
 
     # --- main timed region (CPO path), barrier + sync on both sides, max over ranks
     for _ in range(args.warmup):
-        step_cpo()
+        g_cpo.replay()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        t_ms, t_enc_ms = timed(step_cpo, args.steps, 0)
+        t_ms = timed(g_cpo, args.steps, 0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t_conv_ms = t_ms - t_enc_ms
     tmax = t_ms
     if world > 1:
         tt = torch.tensor([t_ms], device=dev)
@@ -254,9 +250,12 @@ def run_ours(args):
     flops_step = dense_flops(d, Oh, Ow)
     value = flops_step * args.steps * world / (tmax * 1e-3) / 1e9
 
-    # --- side measurements (same process, rank 0 reports)
-    t_cps, t_cps_enc = timed(step_cps, args.steps, 1)
-    t_i2c, _ = timed(step_im2col, args.steps, 1, split=False)
+    # --- per-kernel breakdown and the other algorithms (same process)
+    t_enc_ms = timed(g_cpo_enc, args.steps, 1)
+    t_conv_ms = timed(g_cpo_conv, args.steps, 1)
+    t_cps = timed(g_cps, args.steps, 1)
+    t_cps_enc = timed(g_cps_enc, args.steps, 1)
+    t_i2c = timed(g_i2c, args.steps, 1)
 
     # encoding sizes, CR (paper units: elements of ptr + DA + IN vs S_im2col)
     pl_, dl_, il_ = spc.spc_encoding_lengths(enc)
@@ -299,23 +298,17 @@ def run_ours(args):
                 "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs, "traffic": None,
                 "peak_source": peak_src, "algorithmic_bytes": enc_bytes}
 
-    # --- end to end through the public API with host buffers (pinned), copies in the timed region
+    # --- end to end through the public API with host buffers: pinned H2D of the
+    # input, encode + conv, D2H of the output, all inside the timed region
     xh = torch.from_numpy(x).pin_memory()
     yh = torch.empty(y.shape, dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        xg.copy_(xh, non_blocking=True); step_cpo(); yh.copy_(y, non_blocking=True)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_ms = 0.0
-    for _ in range(args.steps):
-        flush.zero_()
-        e0.record(stream)
+
+    def e2e_step():
         xg.copy_(xh, non_blocking=True)
-        step_cpo()
+        L_cpo.forward(xg, "cpo")
         yh.copy_(y, non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms += e0.elapsed_time(e1)
+    g_e2e = L_cpo.capture(e2e_step)
+    e2e_ms = timed(g_e2e, args.steps, 2)
     if world > 1:
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -367,8 +360,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--cpu-budget", type=float, default=10.0)

@@ -401,16 +401,15 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
     a.inc = reinterpret_cast<long long*>(base + L.inc);
     a.ntiles = (int)enc_tiles(g);
     size_t smem = enc_smem_bytes(g);
-    cudaError_t err;
-    if (cps) {
-        err = cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static size_t attr_bytes[2] = {0, 0};
+    if (attr_bytes[cps] < smem) {
+        cudaError_t err = cps ? cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                              : cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
-        encode_kernel<true><<<a.ntiles, kEncWarps * 32, smem, st>>>(a);
-    } else {
-        err = cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        encode_kernel<false><<<a.ntiles, kEncWarps * 32, smem, st>>>(a);
+        attr_bytes[cps] = smem;
     }
+    if (cps) encode_kernel<true><<<a.ntiles, kEncWarps * 32, smem, st>>>(a);
+    else encode_kernel<false><<<a.ntiles, kEncWarps * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 

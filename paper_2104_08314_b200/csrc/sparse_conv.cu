@@ -21,6 +21,10 @@
 //    channel's taps held in registers (w[KPL][R][S]);
 //  * the GENERIC variant (any R, S, stride) runs the same pipeline with smem
 //    accumulators and runtime tap loops.
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace spc {
@@ -49,75 +53,84 @@ cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaSt
 
 constexpr int kMaxS = 8;
 
-// Block directory of one channel, from its ptr segment (Alg. 2 lines 9-20).
-// pos[t]: index in ptr of the first count of block t (NOP: a, a+b), -1 when the
-// block is absent or NPF; da[t]: DA offset of the block inside the channel.
+// Block directory of one channel, from its ptr segment `seg` (Alg. 2 lines
+// 9-20).  pos[t]: position in seg of the first count of block t (NOP: a, a+b),
+// -1 when the block is absent or NPF; da[t]: DA offset of block t inside the
+// channel.  Works on a global or a shared-memory copy of the segment.
 struct ChanDir {
     int npc;
     int pos[kMaxS];
     int da[kMaxS];
 };
 
-__device__ __forceinline__ void parse_channel(const Geom& g, const int32_t* __restrict__ ptr, long long P,
-                                              ChanDir& d) {
+__device__ __forceinline__ void parse_channel_rel(const Geom& g, const int32_t* seg, ChanDir& d) {
+#pragma unroll
     for (int t = 0; t < kMaxS; t++) { d.pos[t] = -1; d.da[t] = 0; }
-    const int32_t first = __ldg(ptr + P);
-    d.npc = (first == SPC_NPC);
+    d.npc = (seg[0] == SPC_NPC);                 // skip channel
     if (d.npc) return;
-    if (g.S == 1) {
-        d.pos[0] = (int)(P + 1);
+    if (g.S == 1) {                              // SI Alg. 5: [0, c_0 .. c_{Ow-1}]
+        d.pos[0] = 1;
         return;
     }
-    long long p = P;
-    int dacur = 0;
-    if (g.pl == 0) {                       // NOP [0, a, a+b]
-        d.pos[0] = (int)(p + 1);
-        dacur = __ldg(ptr + p + 2);
-        p += 3;
+    int p = 0, dacur = 0;
+    if (g.pl == 0) {                             // NOP [0, a, a+b]
+        d.pos[0] = 1;
+        dacur = seg[2];
+        p = 3;
     }
+#pragma unroll 1
     for (int t = max(1, g.pl); t <= g.S - 1; t++) {
-        const int32_t f = __ldg(ptr + p + 1);
-        if (f == SPC_NPF) {                // skip pointer
+        if (seg[p + 1] == SPC_NPF) {            // skip pointer
             p += 2;
             continue;
         }
-        d.pos[t] = (int)(p + 1);
+        d.pos[t] = p + 1;
         d.da[t] = dacur;
         const int last = (t < g.S - 1) ? (g.Ow1 - 1 - t) : (g.Ow1 - g.S);
-        dacur += __ldg(ptr + p + 1 + last);
+        dacur += seg[p + 1 + last];
         p += 1 + g.Ow1;
     }
 }
 
-// DA range [lo, hi) (channel-relative) and local column of padded column w.
-__device__ __forceinline__ void column_range(const Geom& g, const int32_t* __restrict__ ptr, const ChanDir& d,
-                                             int w, int& lo, int& hi) {
+__device__ __forceinline__ void parse_channel(const Geom& g, const int32_t* __restrict__ ptr, long long P,
+                                              ChanDir& d) {
+    parse_channel_rel(g, ptr + P, d);
+}
+
+// DA range [lo, hi) (channel-relative) of padded column w.
+__device__ __forceinline__ void column_range_rel(const Geom& g, const int32_t* seg, const ChanDir& d, int w,
+                                                 int& lo, int& hi) {
     lo = hi = 0;
     if (w < 0 || w >= g.Wp) return;
-    if (g.S == 1) {                                           // SI Alg. 5: channel-cumulative
-        lo = (w == 0) ? 0 : __ldg(ptr + d.pos[0] + w - 1);
-        hi = __ldg(ptr + d.pos[0] + w);
+    if (g.S == 1) {                                           // channel-cumulative counts
+        lo = (w == 0) ? 0 : seg[d.pos[0] + w - 1];
+        hi = seg[d.pos[0] + w];
         return;
     }
     if (w >= g.S - 1 && w <= g.Wp - g.S) {                    // overlapK_w column of partition s
         const int t = g.S - 1, s = w - g.S + 1;
         if (d.pos[t] < 0) return;
-        lo = d.da[t] + ((s == 0) ? 0 : __ldg(ptr + d.pos[t] + s - 1));
-        hi = d.da[t] + __ldg(ptr + d.pos[t] + s);
+        lo = d.da[t] + ((s == 0) ? 0 : seg[d.pos[t] + s - 1]);
+        hi = d.da[t] + seg[d.pos[t] + s];
         return;
     }
     const bool left = w < g.S - 1;
     const int t = left ? w : (g.Wp - 1 - w);
     if (t < g.pl || d.pos[t] < 0) return;                    // pad column or NPF block
     if (t == 0) {                                             // NOP: col 0 then col Wp-1
-        const int a = __ldg(ptr + d.pos[0]);
+        const int a = seg[d.pos[0]];
         if (left) { lo = 0; hi = a; }
-        else { lo = a; hi = __ldg(ptr + d.pos[0] + 1); }
+        else { lo = a; hi = seg[d.pos[0] + 1]; }
         return;
     }
-    const int c0 = __ldg(ptr + d.pos[t]);                     // left column owned by partition 0
+    const int c0 = seg[d.pos[t]];                             // left column owned by partition 0
     if (left) { lo = d.da[t]; hi = d.da[t] + c0; }
-    else { lo = d.da[t] + c0; hi = d.da[t] + __ldg(ptr + d.pos[t] + g.Ow1 - 1 - t); }
+    else { lo = d.da[t] + c0; hi = d.da[t] + seg[d.pos[t] + g.Ow1 - 1 - t]; }
+}
+
+__device__ __forceinline__ void column_range(const Geom& g, const int32_t* __restrict__ seg, const ChanDir& d,
+                                             int w, int& lo, int& hi) {
+    column_range_rel(g, seg, d, w, lo, hi);
 }
 
 // -------------------------------------------------------- CPS expansion
@@ -208,16 +221,28 @@ struct ConvArgs {
     float* __restrict__ y;
     int relu;
     int tiles_x;
+    int cg;     // CTAs per cluster splitting the input channels
+    int pmax;   // longest ptr segment of one channel
 };
 
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int WARPS_>
+// Tile configuration of the register-tile kernel.
+//   TY x TX outputs per CTA, KPL output channels per lane, KG k-groups of 32*KPL
+//   channels and CS channel splits per CTA (WARPS = KG*CS), CH channels staged
+//   per chunk.
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int KG_, int CS_, int CH_>
 struct TileCfg {
-    static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_, WARPS = WARPS_;
-    static constexpr int WH = (TY - 1) * SH + R;   // input window rows
-    static constexpr int WW = (TX - 1) * SW + S;   // input window cols
+    static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
+    static constexpr int KG = KG_, CS = CS_, CH = CH_;
+    static constexpr int WARPS = KG * CS, THREADS = 32 * WARPS;
+    static constexpr int KB = 32 * KPL * KG;          // output channels per CTA
+    static constexpr int RS = R * S;
+    static constexpr int NACC = KPL * TY * TX;         // accumulators per lane
+    static constexpr int WH = (TY - 1) * SH + R;       // input window rows
+    static constexpr int WW = (TX - 1) * SW + S;       // input window cols
     static constexpr int NCASE = WH * WW;
     static_assert(WW <= 32, "window columns are mapped to lanes");
     static_assert(NCASE <= 256, "jump table size");
+    static_assert(NACC % 32 == 0, "reduction pieces of 32 accumulators");
 };
 
 // One NZE at window position CASE = hr*WW + wr: static FFMAs into acc.
@@ -255,19 +280,20 @@ __device__ __forceinline__ void dispatch(int cs, float v, float (&acc)[T::KPL][T
     switch (cs) {
         SPC_C256(0)
         default:
-            break;
+            __builtin_unreachable();
     }
 }
 
 // Builds the list of NZEs of one channel that fall in the window
-// [hy0, hy0+WH) x [wx0, wx0+WW) (padded coordinates); returns its length.
-// lanes j < WW own window column wx0 + j.
-__device__ __forceinline__ int build_list(const ConvArgs& a, const ChanDir& d, long long Z, int hy0, int wx0,
+// [hy0, hy0+WH) x [wx0, wx0+WW) (padded coordinates) from global memory;
+// returns its length (generic kernel).  lanes j < WW own window column wx0 + j.
+__device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg, const ChanDir& d, long long Z,
+                                          int hy0, int wx0,
                                           int WH, int WW, float2* list) {
     const Geom& g = a.g;
     const int lane = threadIdx.x & 31;
     int lo = 0, hi = 0;
-    if (lane < WW) column_range(g, a.ptr, d, wx0 + lane, lo, hi);
+    if (lane < WW) column_range(g, seg, d, wx0 + lane, lo, hi);
     int n = 0;
     unsigned nonempty = __ballot_sync(0xffffffffu, hi > lo);
     while (nonempty) {
@@ -289,7 +315,6 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const ChanDir& d, l
                 list[pos] = make_float2(__ldg(a.da + Z + i), __int_as_float((h - hy0) * WW + j));
             }
             n += __popc(km);
-            // rows ascend within a column: stop once the chunk passed the window
             if (__shfl_sync(0xffffffffu, h, 31) >= hy0 + WH && b + 32 < chi) break;
         }
     }
@@ -297,19 +322,39 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const ChanDir& d, l
     return n;
 }
 
+// Register-tile kernel.  Per chunk of CH input channels:
+//  P0  stage the chunk's ptr segments (contiguous in the stream), DA offsets and
+//      the taps W[c][l][m][kbase..kbase+KB) in shared memory (coalesced);
+//  P1  one warp per channel: block directory from the staged ptr (NPC/NPF skip),
+//      DA ranges of the window columns, then all window NZEs loaded with many
+//      loads in flight, rows filtered, compacted into the channel's smem list;
+//  P2  warp (kg, cs) replays the lists of channels cs, cs+CS, ... with
+//      jump-table dispatch into register accumulators.
+// Epilogue: reduce the CS warps through smem, then the cg CTAs of the cluster
+// through distributed shared memory; ReLU; coalesced NKHW store.
 template <class T>
-__global__ void __launch_bounds__(T::WARPS * 32) sparse_conv_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
+    namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
-    constexpr int KB = 32 * T::KPL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = blockIdx.z;
-    const int kbase = blockIdx.y * KB;
+    const int kg = warp / T::CS, cs = warp % T::CS;
+    const int n = blockIdx.z / a.cg;
+    const int rank = (a.cg > 1) ? (int)cgrp::this_cluster().block_rank() : 0;
+    const int kbase = blockIdx.y * T::KB;
     const int tyi = blockIdx.x / a.tiles_x, txi = blockIdx.x % a.tiles_x;
     const int oy0 = tyi * T::TY, ox0 = txi * T::TX;
     const int hy0 = oy0 * T::SH, wx0 = ox0 * T::SW;
+    const int cper = (g.C + a.cg - 1) / a.cg;
+    const int c_begin = rank * cper, c_end = min(g.C, c_begin + cper);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* list = reinterpret_cast<float2*>(smem_raw) + warp * T::NCASE;
+    float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
+    float2* s_list = reinterpret_cast<float2*>(s_w + T::CH * T::RS * T::KB);          // [CH][NCASE]
+    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * T::NCASE);                   // [CH * pmax]
+    int* s_poff = s_ptr + T::CH * a.pmax;                                             // [CH]
+    int* s_cnt = s_poff + T::CH;                                                      // [CH]
+    int* s_scr = s_cnt + T::CH;                                                       // [WARPS][2][32]
+    long long* s_z = reinterpret_cast<long long*>(s_scr + T::WARPS * 64);             // [CH]
 
     float acc[T::KPL][T::TY][T::TX];
 #pragma unroll
@@ -319,57 +364,149 @@ __global__ void __launch_bounds__(T::WARPS * 32) sparse_conv_kernel(ConvArgs a) 
 #pragma unroll
             for (int xx = 0; xx < T::TX; xx++) acc[kk][yy][xx] = 0.f;
 
-    for (int c = warp; c < g.C; c += T::WARPS) {
-        const long long nc = (long long)n * g.C + c;
-        ChanDir d;
-        parse_channel(g, a.ptr, a.cpo_off[nc], d);   // NPC -> skip channel
-        if (d.npc) continue;
-        const long long Z = a.cnz_off[nc];
-        const int cnt = build_list(a, d, Z, hy0, wx0, T::WH, T::WW, list);
-        if (cnt == 0) continue;
-        float w[T::KPL][T::R][T::S];
-#pragma unroll
-        for (int kk = 0; kk < T::KPL; kk++) {
-            const int k = kbase + kk * 32 + lane;
-#pragma unroll
-            for (int l = 0; l < T::R; l++)
-#pragma unroll
-                for (int m = 0; m < T::S; m++)
-                    w[kk][l][m] = (k < g.K) ? __ldg(a.wp + (((long long)c * T::R + l) * T::S + m) * g.K + k) : 0.f;
+    for (int c0 = c_begin; c0 < c_end; c0 += T::CH) {
+        const int chn = min(T::CH, c_end - c0);
+        const long long nc0 = (long long)n * g.C + c0;
+        // ---- P0: stage ptr segments, DA offsets, taps
+        const long long pbase = __ldg(a.cpo_off + nc0);
+        const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
+        for (int i = threadIdx.x; i < plen; i += T::THREADS) s_ptr[i] = __ldg(a.ptr + pbase + i);
+        for (int j = threadIdx.x; j < chn; j += T::THREADS) {
+            s_poff[j] = (int)(__ldg(a.cpo_off + nc0 + j) - pbase);
+            s_z[j] = __ldg(a.cnz_off + nc0 + j);
         }
+        for (int i = threadIdx.x; i < chn * T::RS * T::KB; i += T::THREADS) {
+            const int kk = i % T::KB, crs = i / T::KB;         // crs = j*RS + rs
+            const int k = kbase + kk;
+            s_w[i] = (k < g.K) ? __ldg(a.wp + ((long long)c0 * T::RS + crs) * g.K + k) : 0.f;
+        }
+        __syncthreads();
+        // ---- P1: window NZE lists, one warp per channel
+        for (int j = warp; j < chn; j += T::WARPS) {
+            ChanDir d;
+            parse_channel_rel(g, s_ptr + s_poff[j], d);
+            int lo = 0, hi = 0;
+            if (!d.npc && lane < T::WW) column_range_rel(g, s_ptr + s_poff[j], d, wx0 + lane, lo, hi);
+            int tot;
+            const int pre = warp_exclusive_scan(hi - lo, &tot);
+            int* spre = s_scr + warp * 64;
+            int* slo = spre + 32;
+            spre[lane] = (lane < T::WW) ? pre : (1 << 30);
+            slo[lane] = lo;
+            __syncwarp();
+            const long long Z = s_z[j];
+            float2* lst = s_list + j * T::NCASE;
+            int cnt = 0;
+            for (int f0 = 0; f0 < tot; f0 += 128) {
+                int e[4], col[4];
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int f = f0 + 32 * u + lane;
+                    col[u] = 0;
+                    e[u] = -1;
+                    v[u] = 0.f;
+                    if (f < tot) {
+                        // last window column whose prefix <= f (branchless binary search, WW <= 32)
+                        int jc = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                        col[u] = jc;
+                        const long long idx = Z + slo[jc] + (f - spre[jc]);
+                        e[u] = __ldg(a.in + idx);
+                        v[u] = __ldg(a.da + idx);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int h = e[u] / T::S;     // IN = L + h*S with L < S
+                    const bool keep = e[u] >= 0 && h >= hy0 && h < hy0 + T::WH;
+                    const unsigned km = __ballot_sync(0xffffffffu, keep);
+                    if (keep)
+                        lst[cnt + __popc(km & lanemask_lt())] =
+                            make_float2(v[u], __int_as_float((h - hy0) * T::WW + col[u]));
+                    cnt += __popc(km);
+                }
+            }
+            if (lane == 0) s_cnt[j] = cnt;
+            __syncwarp();
+        }
+        __syncthreads();
+        // ---- P2: FFMA replay
+        for (int j = cs; j < chn; j += T::CS) {
+            const int cnt = s_cnt[j];
+            if (cnt == 0) continue;
+            float w[T::KPL][T::R][T::S];
+#pragma unroll
+            for (int kk = 0; kk < T::KPL; kk++)
+#pragma unroll
+                for (int l = 0; l < T::R; l++)
+#pragma unroll
+                    for (int m = 0; m < T::S; m++)
+                        w[kk][l][m] = s_w[(j * T::RS + l * T::S + m) * T::KB + (kg * T::KPL + kk) * 32 + lane];
+            const float2* lst = s_list + j * T::NCASE;
 #pragma unroll 2
-        for (int e = 0; e < cnt; e++) {
-            const float2 it = list[e];
-            dispatch<T>(__float_as_int(it.y), it.x, acc, w);
+            for (int e = 0; e < cnt; e++) {
+                const float2 it = lst[e];
+                dispatch<T>(__float_as_int(it.y), it.x, acc, w);
+            }
         }
-        __syncwarp();
+        __syncthreads();
     }
 
-    // ---- reduce the WARPS channel splits through smem, store NKHW coalesced over x
-    __syncthreads();
-    float* red = reinterpret_cast<float*>(smem_raw);   // [WARPS][KPL*TY*TX][32]
-    constexpr int NACC = T::KPL * T::TY * T::TX;
+    // ---- epilogue 1: reduce the CS channel splits (pieces of 32 accumulators)
+    float* flat = &acc[0][0][0];
+    float* red = s_w;   // [CS][KG][32][32]
+    if constexpr (T::CS > 1) {
 #pragma unroll
-    for (int kk = 0; kk < T::KPL; kk++)
+        for (int p = 0; p < T::NACC / 32; p++) {
+            if (cs > 0) {
 #pragma unroll
-        for (int yy = 0; yy < T::TY; yy++)
+                for (int i = 0; i < 32; i++) red[((cs * T::KG + kg) * 32 + i) * 32 + lane] = flat[p * 32 + i];
+            }
+            __syncthreads();
+            if (cs == 0) {
 #pragma unroll
-            for (int xx = 0; xx < T::TX; xx++)
-                red[((size_t)warp * NACC + (kk * T::TY + yy) * T::TX + xx) * 32 + lane] = acc[kk][yy][xx];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < KB * T::TY * T::TX; idx += T::WARPS * 32) {
-        const int xx = idx % T::TX;
-        const int yy = (idx / T::TX) % T::TY;
-        const int kl = idx / (T::TX * T::TY);        // 0..KB-1
-        const int kk = kl / 32, ln = kl % 32;
-        const int k = kbase + kl, oy = oy0 + yy, ox = ox0 + xx;
+                for (int i = 0; i < 32; i++) {
+                    float s = flat[p * 32 + i];
+                    for (int q = 1; q < T::CS; q++) s += red[((q * T::KG + kg) * 32 + i) * 32 + lane];
+                    flat[p * 32 + i] = s;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // ---- epilogue 2: CTA partial -> smem [KG][KPL][32 lanes][TY*TX + 1]
+    constexpr int TT = T::TY * T::TX, TP = TT + 1;
+    float* part = s_w;
+    if (cs == 0) {
+#pragma unroll
+        for (int kk = 0; kk < T::KPL; kk++)
+#pragma unroll
+            for (int t = 0; t < TT; t++) part[((kg * T::KPL + kk) * 32 + lane) * TP + t] = acc[kk][t / T::TX][t % T::TX];
+    }
+    if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
+    // ---- epilogue 3: sum the cluster's partials (DSMEM), ReLU, store NKHW
+    const int total = T::KB * TT;
+    const int per = (total + a.cg - 1) / a.cg;
+    const int i0 = rank * per, i1 = min(total, i0 + per);
+    for (int i = i0 + threadIdx.x; i < i1; i += T::THREADS) {
+        const int t = i % TT, kl = i / TT;        // kl = (kg*KPL + kk)*32 + lane
+        const int k = kbase + kl, oy = oy0 + t / T::TX, ox = ox0 + t % T::TX;
+        const int sidx = kl * TP + t;
+        float s = part[sidx];
+        if (a.cg > 1) {
+            for (int r = 0; r < a.cg; r++) {
+                if (r == rank) continue;
+                s += *cgrp::this_cluster().map_shared_rank(part + sidx, r);
+            }
+        }
         if (k >= g.K || oy >= g.Oh || ox >= g.Ow) continue;
-        float s = 0.f;
-#pragma unroll
-        for (int wv = 0; wv < T::WARPS; wv++) s += red[((size_t)wv * NACC + (kk * T::TY + yy) * T::TX + xx) * 32 + ln];
         if (a.relu) s = fmaxf(s, 0.f);
         a.y[(((long long)n * g.K + k) * g.Oh + oy) * g.Ow + ox] = s;
     }
+    if (a.cg > 1) cgrp::this_cluster().sync();
 }
 
 // Generic variant: any R, S, stride; TY x TX = 4 x 4 tile, accumulators in smem.
@@ -393,10 +530,11 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
     for (int c = warp; c < g.C; c += kGenWarps) {
         const long long nc = (long long)n * g.C + c;
         ChanDir d;
-        parse_channel(g, a.ptr, a.cpo_off[nc], d);
+        const int32_t* seg = a.ptr + a.cpo_off[nc];
+        parse_channel_rel(g, seg, d);
         if (d.npc) continue;
         const long long Z = a.cnz_off[nc];
-        const int cnt = build_list(a, d, Z, hy0, wx0, WH, WW, list);
+        const int cnt = build_list(a, seg, d, Z, hy0, wx0, WH, WW, list);
         for (int e = 0; e < cnt; e++) {
             const float2 it = list[e];
             const int cs = __float_as_int(it.y);
@@ -429,19 +567,52 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
 }
 
 template <class T>
-static cudaError_t run_tiled(ConvArgs& a, cudaStream_t st) {
+static size_t tiled_smem(const ConvArgs& a) {
+    size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * T::NCASE * 8 + (size_t)T::CH * a.pmax * 4 +
+                  (size_t)2 * T::CH * 4 + (size_t)T::WARPS * 64 * 4 + 16 + (size_t)T::CH * 8;
+    size_t red = (size_t)T::CS * T::KG * 32 * 32 * 4;
+    size_t part = (size_t)T::KB * (T::TY * T::TX + 1) * 4;
+    return std::max(main, std::max(red, part));
+}
+
+template <class T>
+static cudaError_t run_tiled(ConvArgs& a, int cg, cudaStream_t st) {
     const Geom& g = a.g;
     const int tx = (g.Ow + T::TX - 1) / T::TX, ty = (g.Oh + T::TY - 1) / T::TY;
     a.tiles_x = tx;
-    const int kgroups = (g.K + 32 * T::KPL - 1) / (32 * T::KPL);
-    size_t list_bytes = (size_t)T::WARPS * T::NCASE * sizeof(float2);
-    size_t red_bytes = (size_t)T::WARPS * T::KPL * T::TY * T::TX * 32 * sizeof(float);
-    size_t smem = list_bytes > red_bytes ? list_bytes : red_bytes;
-    cudaError_t err = cudaFuncSetAttribute(sparse_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    dim3 grid(tx * ty, kgroups, g.N);
-    sparse_conv_kernel<T><<<grid, T::WARPS * 32, smem, st>>>(a);
-    return cudaGetLastError();
+    a.cg = cg;
+    const int kblocks = (g.K + T::KB - 1) / T::KB;
+    const size_t smem = tiled_smem<T>(a);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    static bool attr_set = false;     // per instantiation
+    static size_t attr_bytes = 0;
+    if (!attr_set || attr_bytes < smem) {
+        cudaError_t err = cudaFuncSetAttribute(sparse_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)std::max(smem, attr_bytes));
+        if (err != cudaSuccess) return err;
+        attr_set = true;
+        attr_bytes = std::max(smem, attr_bytes);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tx * ty, kblocks, g.N * cg);
+    cfg.blockDim = dim3(T::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = cg;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, sparse_conv_kernel<T>, a);
+}
+
+// Pick the channel split across a cluster so that the grid covers the GPU.
+static int pick_cg(long long ctas, int C) {
+    int cg = 1;
+    while (cg < 8 && ctas * cg < 2 * 148 && C >= 16 * cg * 2) cg *= 2;
+    return cg;
 }
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
@@ -457,17 +628,27 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.y = y;
     a.relu = relu;
     a.tiles_x = 1;
-    const bool k_big = g.K > 32;
+    a.cg = 1;
+    a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
+    auto ctas = [&](int TY, int TX, int KB) {
+        return (long long)((g.Oh + TY - 1) / TY) * ((g.Ow + TX - 1) / TX) * ((g.K + KB - 1) / KB) * g.N;
+    };
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        if (k_big) return run_tiled<TileCfg<3, 3, 1, 1, 8, 8, 2, 4>>(a, st);
-        return run_tiled<TileCfg<3, 3, 1, 1, 8, 8, 1, 4>>(a, st);
+        using T = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16>;
+        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
     }
     if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
-        if (k_big) return run_tiled<TileCfg<3, 3, 2, 2, 4, 8, 2, 4>>(a, st);
-        return run_tiled<TileCfg<3, 3, 2, 2, 4, 8, 1, 4>>(a, st);
+        using T = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 8, 16>;
+        return run_tiled<T>(a, pick_cg(ctas(4, 8, T::KB), g.C), st);
     }
-    if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1) return run_tiled<TileCfg<1, 7, 1, 1, 8, 8, 2, 4>>(a, st);
-    if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1) return run_tiled<TileCfg<7, 1, 1, 1, 8, 8, 2, 4>>(a, st);
+    if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1) {
+        using T = TileCfg<1, 7, 1, 1, 8, 8, 2, 1, 8, 16>;
+        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
+    }
+    if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1) {
+        using T = TileCfg<7, 1, 1, 1, 8, 8, 2, 1, 8, 16>;
+        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
+    }
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
     if (WW > 32) return cudaErrorInvalidValue;
