@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "dispatch_gen.cuh"
 
 namespace spc {
 
@@ -243,45 +244,21 @@ struct TileCfg {
     static_assert(WW <= 32, "window columns are mapped to lanes");
     static_assert(NCASE <= 256, "jump table size");
     static_assert(NACC % 32 == 0, "reduction pieces of 32 accumulators");
+    using RP = Replay<R, S, SH, SW, TY, TX, KPL>;
+    using Word = typename RP::Word;                     // f32x2 pair (k, k+32) or f32
+    static constexpr int NP = RP::kPacked ? KPL / 2 : KPL;
 };
 
-// One NZE at window position CASE = hr*WW + wr: static FFMAs into acc.
-template <class T, int CASE>
-__device__ __forceinline__ void apply_case(float v, float (&acc)[T::KPL][T::TY][T::TX],
-                                           const float (&w)[T::KPL][T::R][T::S]) {
-    constexpr int hr = CASE / T::WW, wr = CASE % T::WW;
-#pragma unroll
-    for (int l = 0; l < T::R; ++l) {
-#pragma unroll
-        for (int m = 0; m < T::S; ++m) {
-            const int y1 = hr - l, x1 = wr - m;
-            if (y1 >= 0 && x1 >= 0 && (y1 % T::SH) == 0 && (x1 % T::SW) == 0 && y1 / T::SH < T::TY &&
-                x1 / T::SW < T::TX) {
-#pragma unroll
-                for (int kk = 0; kk < T::KPL; ++kk)
-                    acc[kk][y1 / T::SH][x1 / T::SW] = fmaf(v, w[kk][l][m], acc[kk][y1 / T::SH][x1 / T::SW]);
-            }
-        }
-    }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
-
-#define SPC_C1(i) \
-    case (i):     \
-        if constexpr ((i) < T::NCASE) apply_case<T, (i)>(v, acc, w); \
-        break;
-#define SPC_C4(i) SPC_C1(i) SPC_C1(i + 1) SPC_C1(i + 2) SPC_C1(i + 3)
-#define SPC_C16(i) SPC_C4(i) SPC_C4(i + 4) SPC_C4(i + 8) SPC_C4(i + 12)
-#define SPC_C64(i) SPC_C16(i) SPC_C16(i + 16) SPC_C16(i + 32) SPC_C16(i + 48)
-#define SPC_C256(i) SPC_C64(i) SPC_C64(i + 64) SPC_C64(i + 128) SPC_C64(i + 192)
-
-template <class T>
-__device__ __forceinline__ void dispatch(int cs, float v, float (&acc)[T::KPL][T::TY][T::TX],
-                                         const float (&w)[T::KPL][T::R][T::S]) {
-    switch (cs) {
-        SPC_C256(0)
-        default:
-            __builtin_unreachable();
-    }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
 
 // Builds the list of NZEs of one channel that fall in the window
@@ -356,30 +333,41 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
     int* s_scr = s_cnt + T::CH;                                                       // [WARPS][2][32]
     long long* s_z = reinterpret_cast<long long*>(s_scr + T::WARPS * 64);             // [CH]
 
-    float acc[T::KPL][T::TY][T::TX];
+    typename T::Word acc[T::NP][T::TY][T::TX];
 #pragma unroll
-    for (int kk = 0; kk < T::KPL; kk++)
+    for (int p = 0; p < T::NP; p++)
 #pragma unroll
         for (int yy = 0; yy < T::TY; yy++)
 #pragma unroll
-            for (int xx = 0; xx < T::TX; xx++) acc[kk][yy][xx] = 0.f;
+            for (int xx = 0; xx < T::TX; xx++) acc[p][yy][xx] = 0;
+    const bool w16 = (g.K % 4) == 0;
 
     for (int c0 = c_begin; c0 < c_end; c0 += T::CH) {
         const int chn = min(T::CH, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
-        // ---- P0: stage ptr segments, DA offsets, taps
+        // ---- P0: stage ptr segments, DA offsets, taps (cp.async: all copies in flight at once)
         const long long pbase = __ldg(a.cpo_off + nc0);
         const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
-        for (int i = threadIdx.x; i < plen; i += T::THREADS) s_ptr[i] = __ldg(a.ptr + pbase + i);
+        for (int i = threadIdx.x; i < plen; i += T::THREADS) cp_async4(s_ptr + i, a.ptr + pbase + i, 4);
         for (int j = threadIdx.x; j < chn; j += T::THREADS) {
             s_poff[j] = (int)(__ldg(a.cpo_off + nc0 + j) - pbase);
             s_z[j] = __ldg(a.cnz_off + nc0 + j);
         }
-        for (int i = threadIdx.x; i < chn * T::RS * T::KB; i += T::THREADS) {
-            const int kk = i % T::KB, crs = i / T::KB;         // crs = j*RS + rs
-            const int k = kbase + kk;
-            s_w[i] = (k < g.K) ? __ldg(a.wp + ((long long)c0 * T::RS + crs) * g.K + k) : 0.f;
+        if (w16) {
+            for (int i = threadIdx.x; i < chn * T::RS * (T::KB / 4); i += T::THREADS) {
+                const int kq = (i % (T::KB / 4)) * 4, crs = i / (T::KB / 4);
+                const int k = kbase + kq;
+                const int nb = max(0, min(16, 4 * (g.K - k)));
+                cp_async16(s_w + crs * T::KB + kq, a.wp + ((long long)c0 * T::RS + crs) * g.K + (nb ? k : 0), nb);
+            }
+        } else {
+            for (int i = threadIdx.x; i < chn * T::RS * T::KB; i += T::THREADS) {
+                const int kk = i % T::KB, crs = i / T::KB;
+                const int k = kbase + kk;
+                cp_async4(s_w + i, a.wp + ((long long)c0 * T::RS + crs) * g.K + (k < g.K ? k : 0), k < g.K ? 4 : 0);
+            }
         }
+        cp_async_wait_all();
         __syncthreads();
         // ---- P1: window NZE lists, one warp per channel
         for (int j = warp; j < chn; j += T::WARPS) {
@@ -433,30 +421,49 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
             __syncwarp();
         }
         __syncthreads();
-        // ---- P2: FFMA replay
+        // ---- P2: FFMA replay (generated brx.idx jump table, FFMA2 bodies)
         for (int j = cs; j < chn; j += T::CS) {
             const int cnt = s_cnt[j];
             if (cnt == 0) continue;
-            float w[T::KPL][T::R][T::S];
+            typename T::Word w[T::NP][T::R][T::S];
 #pragma unroll
-            for (int kk = 0; kk < T::KPL; kk++)
+            for (int p = 0; p < T::NP; p++)
 #pragma unroll
                 for (int l = 0; l < T::R; l++)
 #pragma unroll
-                    for (int m = 0; m < T::S; m++)
-                        w[kk][l][m] = s_w[(j * T::RS + l * T::S + m) * T::KB + (kg * T::KPL + kk) * 32 + lane];
-            const float2* lst = s_list + j * T::NCASE;
-#pragma unroll 2
-            for (int e = 0; e < cnt; e++) {
-                const float2 it = lst[e];
-                dispatch<T>(__float_as_int(it.y), it.x, acc, w);
-            }
+                    for (int m = 0; m < T::S; m++) {
+                        const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane;
+                        if constexpr (T::RP::kPacked) {
+                            const unsigned lo = __float_as_uint(ws[(kg * T::KPL + 2 * p) * 32]);
+                            const unsigned hi = __float_as_uint(ws[(kg * T::KPL + 2 * p + 1) * 32]);
+                            w[p][l][m] = (unsigned long long)lo | ((unsigned long long)hi << 32);
+                        } else {
+                            w[p][l][m] = ws[(kg * T::KPL + p) * 32];
+                        }
+                    }
+            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + j * T::NCASE), cnt, acc, w);
         }
         __syncthreads();
     }
 
+    // unpack the accumulator words into acc_f[KPL][TY][TX] (k = kbase + (kg*KPL + kk)*32 + lane)
+    float accf[T::KPL][T::TY][T::TX];
+#pragma unroll
+    for (int p = 0; p < T::NP; p++)
+#pragma unroll
+        for (int yy = 0; yy < T::TY; yy++)
+#pragma unroll
+            for (int xx = 0; xx < T::TX; xx++) {
+                if constexpr (T::RP::kPacked) {
+                    accf[2 * p][yy][xx] = __uint_as_float((unsigned)(acc[p][yy][xx] & 0xffffffffull));
+                    accf[2 * p + 1][yy][xx] = __uint_as_float((unsigned)(acc[p][yy][xx] >> 32));
+                } else {
+                    accf[p][yy][xx] = acc[p][yy][xx];
+                }
+            }
+
     // ---- epilogue 1: reduce the CS channel splits (pieces of 32 accumulators)
-    float* flat = &acc[0][0][0];
+    float* flat = &accf[0][0][0];
     float* red = s_w;   // [CS][KG][32][32]
     if constexpr (T::CS > 1) {
 #pragma unroll
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
 #pragma unroll
         for (int kk = 0; kk < T::KPL; kk++)
 #pragma unroll
-            for (int t = 0; t < TT; t++) part[((kg * T::KPL + kk) * 32 + lane) * TP + t] = acc[kk][t / T::TX][t % T::TX];
+            for (int t = 0; t < TT; t++) part[((kg * T::KPL + kk) * 32 + lane) * TP + t] = accf[kk][t / T::TX][t % T::TX];
     }
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
     // ---- epilogue 3: sum the cluster's partials (DSMEM), ReLU, store NKHW
@@ -634,20 +641,32 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         return (long long)((g.Oh + TY - 1) / TY) * ((g.Ow + TX - 1) / TX) * ((g.K + KB - 1) / KB) * g.N;
     };
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        using T = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
+        if (g.K <= 32) {
+            using T = TileCfg<3, 3, 1, 1, 8, 8, 1, 1, 8, 16>;
+            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        }
+        if (g.K <= 64) {
+            using T = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16>;
+            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        }
+        using T = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 8, 16>;
+        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
     }
     if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
+        if (g.K <= 64) {
+            using T = TileCfg<3, 3, 2, 2, 4, 8, 2, 1, 8, 16>;
+            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        }
         using T = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(4, 8, T::KB), g.C), st);
+        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
     }
     if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1) {
         using T = TileCfg<1, 7, 1, 1, 8, 8, 2, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
+        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
     }
     if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1) {
         using T = TileCfg<7, 1, 1, 1, 8, 8, 2, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(8, 8, T::KB), g.C), st);
+        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
     }
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
