@@ -35,9 +35,9 @@ inline Geom make_geom(const spc_conv_desc& d) {
     return g;
 }
 
-// Encoder: four channel planes per CTA (one per warp).
-constexpr int kEncWarps = 4;
-constexpr int kEncMaxPlaneBytes = 200 * 1024 / kEncWarps;  // smem stage per plane
+// Encoder: 8 warps per CTA; G = 1..8 planes per CTA (8/G warps per plane).
+constexpr int kEncWarps = 8;
+constexpr int kEncMaxPlaneBytes = 192 * 1024;  // smem stage of one plane
 
 // Decoupled look-back state of the single-pass encoder (lives in the workspace).
 struct EncState {
@@ -48,7 +48,8 @@ struct EncState {
 
 __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-inline long long enc_tiles(const Geom& g) { return (g.NC + kEncWarps - 1) / kEncWarps; }
+// upper bound on encoder tiles (one plane per CTA), for workspace sizing
+inline long long enc_tiles(const Geom& g) { return g.NC; }
 
 // Workspace layout: [EncState | flags[ntiles] | agg[3*ntiles] | inc[3*ntiles] | cps_in[da_cap]]
 struct WsLayout {

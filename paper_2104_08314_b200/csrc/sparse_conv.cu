@@ -301,14 +301,16 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg,
 
 // Register-tile kernel.  Per chunk of CH input channels:
 //  P0  stage the chunk's ptr segments (contiguous in the stream), DA offsets and
-//      the taps W[c][l][m][kbase..kbase+KB) in shared memory (coalesced);
+//      the taps W[c][l][m][kbase..kbase+KB) in shared memory (cp.async);
 //  P1  one warp per channel: block directory from the staged ptr (NPC/NPF skip),
-//      DA ranges of the window columns, then all window NZEs loaded with many
-//      loads in flight, rows filtered, compacted into the channel's smem list;
-//  P2  warp (kg, cs) replays the lists of channels cs, cs+CS, ... with
-//      jump-table dispatch into register accumulators.
-// Epilogue: reduce the CS warps through smem, then the cg CTAs of the cluster
-// through distributed shared memory; ReLU; coalesced NKHW store.
+//      DA ranges of the window columns, then the window columns' NZEs with many
+//      loads in flight; rows outside the tile window are dropped, the kept ones
+//      compacted and given their window position -> smem list {v, v, case, 0}
+//      closed by a sentinel;
+//  P2  warp (kg, cs) replays the lists of channels cs, cs+CS, ... with the
+//      generated brx.idx / FFMA2 loop into register accumulators.
+// Epilogue: reduce the CS warps through smem (all warps), then the cg CTAs of
+// the cluster through distributed shared memory; ReLU; coalesced NKHW store.
 template <class T>
 __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
@@ -323,15 +325,17 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
     const int hy0 = oy0 * T::SH, wx0 = ox0 * T::SW;
     const int cper = (g.C + a.cg - 1) / a.cg;
     const int c_begin = rank * cper, c_end = min(g.C, c_begin + cper);
+    constexpr int LCAP = T::NCASE + 1;   // list capacity per channel, + sentinel
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
-    float2* s_list = reinterpret_cast<float2*>(s_w + T::CH * T::RS * T::KB);          // [CH][NCASE]
-    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * T::NCASE);                   // [CH * pmax]
+    float4* s_list = reinterpret_cast<float4*>(s_w + T::CH * T::RS * T::KB);          // [CH][LCAP]
+    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * LCAP);                       // [CH * pmax]
     int* s_poff = s_ptr + T::CH * a.pmax;                                             // [CH]
     int* s_cnt = s_poff + T::CH;                                                      // [CH]
     int* s_scr = s_cnt + T::CH;                                                       // [WARPS][2][32]
-    long long* s_z = reinterpret_cast<long long*>(s_scr + T::WARPS * 64);             // [CH]
+    long long* s_z = reinterpret_cast<long long*>(s_scr + T::WARPS * 64 + 2);         // [CH] (8B aligned)
+    s_z = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(s_z) + 7) & ~uintptr_t(7));
 
     typename T::Word acc[T::NP][T::TY][T::TX];
 #pragma unroll
@@ -346,64 +350,76 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
         const int chn = min(T::CH, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
         // ---- P0: stage ptr segments, DA offsets, taps (cp.async: all copies in flight at once)
-        const long long pbase = __ldg(a.cpo_off + nc0);
-        const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
-        for (int i = threadIdx.x; i < plen; i += T::THREADS) cp_async4(s_ptr + i, a.ptr + pbase + i, 4);
-        for (int j = threadIdx.x; j < chn; j += T::THREADS) {
-            s_poff[j] = (int)(__ldg(a.cpo_off + nc0 + j) - pbase);
-            s_z[j] = __ldg(a.cnz_off + nc0 + j);
-        }
-        if (w16) {
-            for (int i = threadIdx.x; i < chn * T::RS * (T::KB / 4); i += T::THREADS) {
-                const int kq = (i % (T::KB / 4)) * 4, crs = i / (T::KB / 4);
-                const int k = kbase + kq;
-                const int nb = max(0, min(16, 4 * (g.K - k)));
-                cp_async16(s_w + crs * T::KB + kq, a.wp + ((long long)c0 * T::RS + crs) * g.K + (nb ? k : 0), nb);
+        {
+            const long long pbase = __ldg(a.cpo_off + nc0);
+            const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
+            const int32_t* src = a.ptr + pbase;
+            for (int i = threadIdx.x; i < plen; i += T::THREADS) cp_async4(s_ptr + i, src + i, 4);
+            if (threadIdx.x < chn) {
+                s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
+                s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
             }
-        } else {
-            for (int i = threadIdx.x; i < chn * T::RS * T::KB; i += T::THREADS) {
-                const int kk = i % T::KB, crs = i / T::KB;
-                const int k = kbase + kk;
-                cp_async4(s_w + i, a.wp + ((long long)c0 * T::RS + crs) * g.K + (k < g.K ? k : 0), k < g.K ? 4 : 0);
+            const float* wsrc = a.wp + (long long)c0 * T::RS * g.K + kbase;   // row (j*RS+rs) at stride K
+            const int rows = chn * T::RS;
+            if (w16) {
+                constexpr int VPR = T::KB / 4;                 // 16-byte vectors per row
+                constexpr int RSTEP = T::THREADS / VPR;
+                const int vq = threadIdx.x % VPR, r0 = threadIdx.x / VPR;
+                const int kq = 4 * vq;
+                const int nb = max(0, min(16, 4 * (g.K - (kbase + kq))));
+                for (int r = r0; r < rows; r += RSTEP)
+                    cp_async16(s_w + r * T::KB + kq, wsrc + (long long)r * g.K + (nb ? kq : 0), nb);
+            } else {
+                for (int i = threadIdx.x; i < rows * T::KB; i += T::THREADS) {
+                    const int kk = i % T::KB, r = i / T::KB;
+                    const bool ok = kbase + kk < g.K;
+                    cp_async4(s_w + i, wsrc + (long long)r * g.K + (ok ? kk : 0), ok ? 4 : 0);
+                }
             }
+            cp_async_wait_all();
         }
-        cp_async_wait_all();
         __syncthreads();
         // ---- P1: window NZE lists, one warp per channel
         for (int j = warp; j < chn; j += T::WARPS) {
+            const int* seg = s_ptr + s_poff[j];
+            float4* lst = s_list + j * LCAP;
             ChanDir d;
-            parse_channel_rel(g, s_ptr + s_poff[j], d);
+            parse_channel_rel(g, seg, d);
             int lo = 0, hi = 0;
-            if (!d.npc && lane < T::WW) column_range_rel(g, s_ptr + s_poff[j], d, wx0 + lane, lo, hi);
+            if (!d.npc && lane < T::WW) column_range_rel(g, seg, d, wx0 + lane, lo, hi);
             int tot;
             const int pre = warp_exclusive_scan(hi - lo, &tot);
             int* spre = s_scr + warp * 64;
             int* slo = spre + 32;
             spre[lane] = (lane < T::WW) ? pre : (1 << 30);
             slo[lane] = lo;
+            const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
+            // contiguous when every window column starts where the flattened prefix says
+            const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
             __syncwarp();
             const long long Z = s_z[j];
-            float2* lst = s_list + j * T::NCASE;
             int cnt = 0;
+            // pass 1: load, keep rows of the tile window, compact {v, h, f}
             for (int f0 = 0; f0 < tot; f0 += 128) {
-                int e[4], col[4];
+                int e[4], ff[4];
                 float v[4];
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const int f = f0 + 32 * u + lane;
-                    col[u] = 0;
+                    ff[u] = f;
                     e[u] = -1;
                     v[u] = 0.f;
                     if (f < tot) {
-                        // last window column whose prefix <= f (branchless binary search, WW <= 32)
-                        int jc = 0;
+                        int idx = lo0 + f;
+                        if (!contig) {
+                            int jc = 0;
 #pragma unroll
-                        for (int step = 16; step > 0; step >>= 1)
-                            if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
-                        col[u] = jc;
-                        const long long idx = Z + slo[jc] + (f - spre[jc]);
-                        e[u] = __ldg(a.in + idx);
-                        v[u] = __ldg(a.da + idx);
+                            for (int step = 16; step > 0; step >>= 1)
+                                if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                            idx = slo[jc] + (f - spre[jc]);
+                        }
+                        e[u] = __ldg(a.in + Z + idx);
+                        v[u] = __ldg(a.da + Z + idx);
                     }
                 }
 #pragma unroll
@@ -413,18 +429,31 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
                     const unsigned km = __ballot_sync(0xffffffffu, keep);
                     if (keep)
                         lst[cnt + __popc(km & lanemask_lt())] =
-                            make_float2(v[u], __int_as_float((h - hy0) * T::WW + col[u]));
+                            make_float4(v[u], __int_as_float(h - hy0), __int_as_float(ff[u]), 0.f);
                     cnt += __popc(km);
                 }
             }
-            if (lane == 0) s_cnt[j] = cnt;
+            __syncwarp();
+            // pass 2: window column of each kept NZE -> replay entry {v, v, case, 0}
+            for (int i = lane; i < cnt; i += 32) {
+                const float4 t = lst[i];
+                const int f = __float_as_int(t.z);
+                int jc = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                lst[i] = make_float4(t.x, t.x, __int_as_float(__float_as_int(t.y) * T::WW + jc), 0.f);
+            }
+            if (lane == 0) {
+                lst[cnt] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
+                s_cnt[j] = cnt;
+            }
             __syncwarp();
         }
         __syncthreads();
         // ---- P2: FFMA replay (generated brx.idx jump table, FFMA2 bodies)
         for (int j = cs; j < chn; j += T::CS) {
-            const int cnt = s_cnt[j];
-            if (cnt == 0) continue;
+            if (s_cnt[j] == 0) continue;
             typename T::Word w[T::NP][T::R][T::S];
 #pragma unroll
             for (int p = 0; p < T::NP; p++)
@@ -441,77 +470,68 @@ __global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
                             w[p][l][m] = ws[(kg * T::KPL + p) * 32];
                         }
                     }
-            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + j * T::NCASE), cnt, acc, w);
+            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + j * LCAP), acc, w);
         }
         __syncthreads();
     }
 
-    // unpack the accumulator words into acc_f[KPL][TY][TX] (k = kbase + (kg*KPL + kk)*32 + lane)
-    float accf[T::KPL][T::TY][T::TX];
+    // ---- epilogue 1: unpack, reduce the CS channel splits (all warps), CTA partial -> part
+    constexpr int TT = T::TY * T::TX, TP = TT + 1;
+    constexpr int PIECE = 64 < T::NACC ? 64 : T::NACC;
+    float* red = s_w;                                              // [CS][KG][PIECE][32]
+    float* part = s_w + (T::CS > 1 ? T::CS * T::KG * PIECE * 32 : 0);   // [KG*KPL*32][TP]
+    float accf[T::NACC];
 #pragma unroll
     for (int p = 0; p < T::NP; p++)
 #pragma unroll
-        for (int yy = 0; yy < T::TY; yy++)
-#pragma unroll
-            for (int xx = 0; xx < T::TX; xx++) {
-                if constexpr (T::RP::kPacked) {
-                    accf[2 * p][yy][xx] = __uint_as_float((unsigned)(acc[p][yy][xx] & 0xffffffffull));
-                    accf[2 * p + 1][yy][xx] = __uint_as_float((unsigned)(acc[p][yy][xx] >> 32));
-                } else {
-                    accf[p][yy][xx] = acc[p][yy][xx];
-                }
+        for (int t = 0; t < TT; t++) {
+            if constexpr (T::RP::kPacked) {
+                accf[(2 * p) * TT + t] = __uint_as_float((unsigned)(acc[p][t / T::TX][t % T::TX] & 0xffffffffull));
+                accf[(2 * p + 1) * TT + t] = __uint_as_float((unsigned)(acc[p][t / T::TX][t % T::TX] >> 32));
+            } else {
+                accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
             }
-
-    // ---- epilogue 1: reduce the CS channel splits (pieces of 32 accumulators)
-    float* flat = &accf[0][0][0];
-    float* red = s_w;   // [CS][KG][32][32]
-    if constexpr (T::CS > 1) {
+        }
+    // accf index i = kk*TT + t  ->  part[((kg*KPL + kk)*32 + lane)*TP + t]
+    if constexpr (T::CS == 1) {
 #pragma unroll
-        for (int p = 0; p < T::NACC / 32; p++) {
-            if (cs > 0) {
+        for (int i = 0; i < T::NACC; i++) part[((kg * T::KPL + i / TT) * 32 + lane) * TP + i % TT] = accf[i];
+    } else {
 #pragma unroll
-                for (int i = 0; i < 32; i++) red[((cs * T::KG + kg) * 32 + i) * 32 + lane] = flat[p * 32 + i];
-            }
+        for (int pc = 0; pc < T::NACC / PIECE; pc++) {
+#pragma unroll
+            for (int i = 0; i < PIECE; i++) red[((cs * T::KG + kg) * PIECE + i) * 32 + lane] = accf[pc * PIECE + i];
             __syncthreads();
-            if (cs == 0) {
+            constexpr int PER = PIECE / T::CS;
+            for (int i = cs * PER; i < (cs + 1) * PER; i++) {
+                float sum = 0.f;
 #pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    float s = flat[p * 32 + i];
-                    for (int q = 1; q < T::CS; q++) s += red[((q * T::KG + kg) * 32 + i) * 32 + lane];
-                    flat[p * 32 + i] = s;
-                }
+                for (int q = 0; q < T::CS; q++) sum += red[((q * T::KG + kg) * PIECE + i) * 32 + lane];
+                const int gi = pc * PIECE + i;
+                part[((kg * T::KPL + gi / TT) * 32 + lane) * TP + gi % TT] = sum;
             }
             __syncthreads();
         }
     }
-    // ---- epilogue 2: CTA partial -> smem [KG][KPL][32 lanes][TY*TX + 1]
-    constexpr int TT = T::TY * T::TX, TP = TT + 1;
-    float* part = s_w;
-    if (cs == 0) {
-#pragma unroll
-        for (int kk = 0; kk < T::KPL; kk++)
-#pragma unroll
-            for (int t = 0; t < TT; t++) part[((kg * T::KPL + kk) * 32 + lane) * TP + t] = accf[kk][t / T::TX][t % T::TX];
-    }
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
-    // ---- epilogue 3: sum the cluster's partials (DSMEM), ReLU, store NKHW
+    // ---- epilogue 2: sum the cluster's partials (DSMEM), ReLU, store NKHW
+    float* peers[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) peers[r] = (r < a.cg && r != rank) ? cgrp::this_cluster().map_shared_rank(part, r) : nullptr;
     const int total = T::KB * TT;
     const int per = (total + a.cg - 1) / a.cg;
     const int i0 = rank * per, i1 = min(total, i0 + per);
     for (int i = i0 + threadIdx.x; i < i1; i += T::THREADS) {
         const int t = i % TT, kl = i / TT;        // kl = (kg*KPL + kk)*32 + lane
-        const int k = kbase + kl, oy = oy0 + t / T::TX, ox = ox0 + t % T::TX;
         const int sidx = kl * TP + t;
-        float s = part[sidx];
-        if (a.cg > 1) {
-            for (int r = 0; r < a.cg; r++) {
-                if (r == rank) continue;
-                s += *cgrp::this_cluster().map_shared_rank(part + sidx, r);
-            }
-        }
+        float sum = part[sidx];
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+            if (peers[r]) sum += peers[r][sidx];
+        const int k = kbase + kl, oy = oy0 + t / T::TX, ox = ox0 + t % T::TX;
         if (k >= g.K || oy >= g.Oh || ox >= g.Ow) continue;
-        if (a.relu) s = fmaxf(s, 0.f);
-        a.y[(((long long)n * g.K + k) * g.Oh + oy) * g.Ow + ox] = s;
+        if (a.relu) sum = fmaxf(sum, 0.f);
+        a.y[(((long long)n * g.K + k) * g.Oh + oy) * g.Ow + ox] = sum;
     }
     if (a.cg > 1) cgrp::this_cluster().sync();
 }
@@ -575,11 +595,13 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
 
 template <class T>
 static size_t tiled_smem(const ConvArgs& a) {
-    size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * T::NCASE * 8 + (size_t)T::CH * a.pmax * 4 +
-                  (size_t)2 * T::CH * 4 + (size_t)T::WARPS * 64 * 4 + 16 + (size_t)T::CH * 8;
-    size_t red = (size_t)T::CS * T::KG * 32 * 32 * 4;
-    size_t part = (size_t)T::KB * (T::TY * T::TX + 1) * 4;
-    return std::max(main, std::max(red, part));
+    const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * (T::NCASE + 1) * 16 +
+                        (size_t)T::CH * a.pmax * 4 + (size_t)2 * T::CH * 4 + (size_t)(T::WARPS * 64 + 2) * 4 + 16 +
+                        (size_t)T::CH * 8;
+    constexpr int PIECE = 64 < T::NACC ? 64 : T::NACC;
+    const size_t red = (T::CS > 1 ? (size_t)T::CS * T::KG * PIECE * 32 * 4 : 0) +
+                       (size_t)T::KB * (T::TY * T::TX + 1) * 4;
+    return std::max(main, red);
 }
 
 template <class T>
