@@ -22,6 +22,8 @@
 //  * the GENERIC variant (any R, S, stride) runs the same pipeline with smem
 //    accumulators and runtime tap loops.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -230,8 +232,9 @@ struct ConvArgs {
 //   TY x TX outputs per CTA, KPL output channels per lane, KG k-groups of 32*KPL
 //   channels and CS channel splits per CTA (WARPS = KG*CS), CH channels staged
 //   per chunk.
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int KG_, int CS_, int CH_>
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int KG_, int CS_, int CH_, int MINB_ = 1>
 struct TileCfg {
+    static constexpr int MINB = MINB_;   // CTAs per SM the register budget targets
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
     static constexpr int KG = KG_, CS = CS_, CH = CH_;
     static constexpr int WARPS = KG * CS, THREADS = 32 * WARPS;
@@ -312,7 +315,7 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg,
 // Epilogue: reduce the CS warps through smem (all warps), then the cg CTAs of
 // the cluster through distributed shared memory; ReLU; coalesced NKHW store.
 template <class T>
-__global__ void __launch_bounds__(T::THREADS) sparse_conv_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -637,11 +640,37 @@ static cudaError_t run_tiled(ConvArgs& a, int cg, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, sparse_conv_kernel<T>, a);
 }
 
-// Pick the channel split across a cluster so that the grid covers the GPU.
-static int pick_cg(long long ctas, int C) {
-    int cg = 1;
-    while (cg < 8 && ctas * cg < 2 * 148 && C >= 16 * cg * 2) cg *= 2;
-    return cg;
+// Channel split across a cluster: the largest cg in {1,2,3,4,6,8} that keeps the
+// grid within one wave of resident CTAs and at least 8 channels per CTA.
+static int pick_cg(long long ctas, int C, int minb) {
+    int best = 1;
+    const int cands[] = {1, 2, 3, 4, 6, 8};
+    for (int cg : cands)
+        if (ctas * cg <= 148LL * minb && C >= 8 * cg) best = cg;
+    return best;
+}
+
+// Development override: SPC_TUNE="<config>:<cg>" (cg 0 = automatic).
+static const char* tune_cfg(int* cg) {
+    static const char* env = getenv("SPC_TUNE");
+    *cg = 0;
+    if (!env) return nullptr;
+    const char* colon = strchr(env, ':');
+    if (colon) *cg = atoi(colon + 1);
+    return env;
+}
+
+template <class T>
+static cudaError_t run_auto(ConvArgs& a, int cg_override, cudaStream_t st) {
+    const Geom& g = a.g;
+    const long long ctas = (long long)((g.Oh + T::TY - 1) / T::TY) * ((g.Ow + T::TX - 1) / T::TX) *
+                           ((g.K + T::KB - 1) / T::KB) * g.N;
+    const int cg = cg_override > 0 ? cg_override : pick_cg(ctas, g.C, T::MINB);
+    return run_tiled<T>(a, cg, st);
+}
+
+static bool tune_is(const char* t, const char* name) {
+    return t && strncmp(t, name, strlen(name)) == 0 && (t[strlen(name)] == ':' || t[strlen(name)] == 0);
 }
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
@@ -659,36 +688,41 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.tiles_x = 1;
     a.cg = 1;
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
-    auto ctas = [&](int TY, int TX, int KB) {
-        return (long long)((g.Oh + TY - 1) / TY) * ((g.Ow + TX - 1) / TX) * ((g.K + KB - 1) / KB) * g.N;
-    };
+    int tcg = 0;
+    const char* t = tune_cfg(&tcg);
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        if (g.K <= 32) {
-            using T = TileCfg<3, 3, 1, 1, 8, 8, 1, 1, 8, 16>;
-            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
-        }
-        if (g.K <= 64) {
-            using T = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16>;
-            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
-        }
-        using T = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        using A = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
+        using B = TileCfg<3, 3, 1, 1, 4, 8, 2, 1, 8, 16, 2>;
+        using C = TileCfg<3, 3, 1, 1, 4, 8, 2, 1, 4, 16, 3>;
+        using D = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 8, 16, 1>;
+        using E = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 4, 16, 2>;
+        using F = TileCfg<3, 3, 1, 1, 8, 8, 1, 1, 8, 16, 1>;
+        if (tune_is(t, "A")) return run_auto<A>(a, tcg, st);
+        if (tune_is(t, "B")) return run_auto<B>(a, tcg, st);
+        if (tune_is(t, "C")) return run_auto<C>(a, tcg, st);
+        if (tune_is(t, "D")) return run_auto<D>(a, tcg, st);
+        if (tune_is(t, "E")) return run_auto<E>(a, tcg, st);
+        if (g.K <= 32) return run_auto<F>(a, tcg, st);
+        if (g.K <= 64) return run_auto<B>(a, tcg, st);
+        return run_auto<E>(a, tcg, st);
     }
     if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
-        if (g.K <= 64) {
-            using T = TileCfg<3, 3, 2, 2, 4, 8, 2, 1, 8, 16>;
-            return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
-        }
-        using T = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        using A = TileCfg<3, 3, 2, 2, 4, 8, 2, 1, 8, 16, 2>;
+        using B = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 8, 16, 1>;
+        using C = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 4, 16, 2>;
+        if (tune_is(t, "A")) return run_auto<A>(a, tcg, st);
+        if (tune_is(t, "B")) return run_auto<B>(a, tcg, st);
+        if (tune_is(t, "C")) return run_auto<C>(a, tcg, st);
+        if (g.K <= 64) return run_auto<A>(a, tcg, st);
+        return run_auto<C>(a, tcg, st);
     }
     if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1) {
-        using T = TileCfg<1, 7, 1, 1, 8, 8, 2, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        using A = TileCfg<1, 7, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
+        return run_auto<A>(a, tcg, st);
     }
     if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1) {
-        using T = TileCfg<7, 1, 1, 1, 8, 8, 2, 1, 8, 16>;
-        return run_tiled<T>(a, pick_cg(ctas(T::TY, T::TX, T::KB), g.C), st);
+        using A = TileCfg<7, 1, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
+        return run_auto<A>(a, tcg, st);
     }
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
