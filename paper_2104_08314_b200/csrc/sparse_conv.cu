@@ -223,32 +223,33 @@ struct ConvArgs {
     const float* __restrict__ wp;        // [C][R][S][K]
     float* __restrict__ y;
     int relu;
-    int tiles_x;
-    int cg;     // CTAs per cluster splitting the input channels
-    int pmax;   // longest ptr segment of one channel
+    int tiles_x;    // generic kernel: tiles per output row
+    int cg;         // CTAs per cluster splitting the input channels
+    int pmax;       // longest ptr segment of one channel
+    int rt;         // strip kernel: row tiles per strip (warps per channel split)
+    int csplit;     // strip kernel: channel splits inside the CTA
 };
 
-// Tile configuration of the register-tile kernel.
-//   TY x TX outputs per CTA, KPL output channels per lane, KG k-groups of 32*KPL
-//   channels and CS channel splits per CTA (WARPS = KG*CS), CH channels staged
-//   per chunk.
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int KG_, int CS_, int CH_, int MINB_ = 1>
-struct TileCfg {
-    static constexpr int MINB = MINB_;   // CTAs per SM the register budget targets
+// Strip-kernel configuration: a CTA owns a column strip of TX output columns and
+// all output rows (rt row tiles of TY rows, one per warp), KPL output channels
+// per lane (pairs (k, k+32) packed for FFMA2 when KPL is even), CH input
+// channels staged per chunk.
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2>
+struct StripCfg {
+    static constexpr int MINB = MINB_;   // CTAs per SM targeted by the register budget
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
-    static constexpr int KG = KG_, CS = CS_, CH = CH_;
-    static constexpr int WARPS = KG * CS, THREADS = 32 * WARPS;
-    static constexpr int KB = 32 * KPL * KG;          // output channels per CTA
+    static constexpr int CH = 8, MAXW = 8, THREADS = 32 * MAXW;
+    static constexpr int KB = 32 * KPL;               // output channels per CTA
     static constexpr int RS = R * S;
-    static constexpr int NACC = KPL * TY * TX;         // accumulators per lane
-    static constexpr int WH = (TY - 1) * SH + R;       // input window rows
-    static constexpr int WW = (TX - 1) * SW + S;       // input window cols
+    static constexpr int NACC = KPL * TY * TX;        // accumulators per lane
+    static constexpr int WH = (TY - 1) * SH + R;      // input window rows of a row tile
+    static constexpr int WW = (TX - 1) * SW + S;      // input window cols of the strip
     static constexpr int NCASE = WH * WW;
+    static constexpr int LCAP = NCASE + 2;            // list slots: entries + sentinel + prefetch pad
+    static constexpr int RSTEP = TY * SH;             // input rows between row tiles
     static_assert(WW <= 32, "window columns are mapped to lanes");
-    static_assert(NCASE <= 256, "jump table size");
-    static_assert(NACC % 32 == 0, "reduction pieces of 32 accumulators");
     using RP = Replay<R, S, SH, SW, TY, TX, KPL>;
-    using Word = typename RP::Word;                     // f32x2 pair (k, k+32) or f32
+    using Word = typename RP::Word;
     static constexpr int NP = RP::kPacked ? KPL / 2 : KPL;
 };
 
@@ -302,43 +303,44 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg,
     return n;
 }
 
-// Register-tile kernel.  Per chunk of CH input channels:
+// Strip kernel.  CTA = (image n, column strip of TX outputs, KB output
+// channels, input-channel range of its cluster rank); warp (r, cs) owns row
+// tile r of the strip for the channels cs, cs+csplit, ...  Per chunk of CH
+// input channels:
 //  P0  stage the chunk's ptr segments (contiguous in the stream), DA offsets and
-//      the taps W[c][l][m][kbase..kbase+KB) in shared memory (cp.async);
-//  P1  one warp per channel: block directory from the staged ptr (NPC/NPF skip),
-//      DA ranges of the window columns, then the window columns' NZEs with many
-//      loads in flight; rows outside the tile window are dropped, the kept ones
-//      compacted and given their window position -> smem list {v, v, case, 0}
-//      closed by a sentinel;
-//  P2  warp (kg, cs) replays the lists of channels cs, cs+CS, ... with the
-//      generated brx.idx / FFMA2 loop into register accumulators.
-// Epilogue: reduce the CS warps through smem (all warps), then the cg CTAs of
-// the cluster through distributed shared memory; ReLU; coalesced NKHW store.
+//      taps W[c][l][m][kbase..+KB) in shared memory (cp.async);
+//  P1  one warp per channel: block directory from the staged ptr (NPC / NPF skip),
+//      DA ranges of the strip's window columns, then every NZE of those columns
+//      (many loads in flight) is bucketed into the list of each row tile whose
+//      window holds it (1 or 2), as a replay entry {v, v, window position, 0};
+//  P2  warp (r, cs) replays its lists (generated brx.idx / FFMA2 loop) into
+//      register accumulators.
+// Epilogue: reduce the csplit warps of a row tile through smem, then the cg
+// CTAs of the cluster through distributed shared memory; ReLU; NKHW store.
 template <class T>
-__global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kg = warp / T::CS, cs = warp % T::CS;
+    const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+    const int RT = a.rt, CS = a.csplit;
+    const int rtile = warp % RT, cs = warp / RT;
     const int n = blockIdx.z / a.cg;
     const int rank = (a.cg > 1) ? (int)cgrp::this_cluster().block_rank() : 0;
     const int kbase = blockIdx.y * T::KB;
-    const int tyi = blockIdx.x / a.tiles_x, txi = blockIdx.x % a.tiles_x;
-    const int oy0 = tyi * T::TY, ox0 = txi * T::TX;
-    const int hy0 = oy0 * T::SH, wx0 = ox0 * T::SW;
+    const int ox0 = blockIdx.x * T::TX, wx0 = ox0 * T::SW;
     const int cper = (g.C + a.cg - 1) / a.cg;
     const int c_begin = rank * cper, c_end = min(g.C, c_begin + cper);
-    constexpr int LCAP = T::NCASE + 1;   // list capacity per channel, + sentinel
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
-    float4* s_list = reinterpret_cast<float4*>(s_w + T::CH * T::RS * T::KB);          // [CH][LCAP]
-    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * LCAP);                       // [CH * pmax]
+    float4* s_list = reinterpret_cast<float4*>(s_w + T::CH * T::RS * T::KB);          // [CH][RT][LCAP]
+    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * RT * T::LCAP);               // [CH * pmax]
     int* s_poff = s_ptr + T::CH * a.pmax;                                             // [CH]
-    int* s_cnt = s_poff + T::CH;                                                      // [CH]
-    int* s_scr = s_cnt + T::CH;                                                       // [WARPS][2][32]
-    long long* s_z = reinterpret_cast<long long*>(s_scr + T::WARPS * 64 + 2);         // [CH] (8B aligned)
-    s_z = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(s_z) + 7) & ~uintptr_t(7));
+    int* s_cnt = s_poff + T::CH;                                                      // [CH][RT]
+    int* s_scr = s_cnt + T::CH * RT;                                                  // [MAXW][64]
+    long long* s_z = reinterpret_cast<long long*>(
+        (reinterpret_cast<uintptr_t>(s_scr + T::MAXW * 64) + 7) & ~uintptr_t(7));      // [CH]
 
     typename T::Word acc[T::NP][T::TY][T::TX];
 #pragma unroll
@@ -352,12 +354,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
     for (int c0 = c_begin; c0 < c_end; c0 += T::CH) {
         const int chn = min(T::CH, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
-        // ---- P0: stage ptr segments, DA offsets, taps (cp.async: all copies in flight at once)
+        // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight)
         {
             const long long pbase = __ldg(a.cpo_off + nc0);
             const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
             const int32_t* src = a.ptr + pbase;
-            for (int i = threadIdx.x; i < plen; i += T::THREADS) cp_async4(s_ptr + i, src + i, 4);
+            for (int i = threadIdx.x; i < plen; i += nthreads) cp_async4(s_ptr + i, src + i, 4);
             if (threadIdx.x < chn) {
                 s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
                 s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
@@ -366,14 +368,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
             const int rows = chn * T::RS;
             if (w16) {
                 constexpr int VPR = T::KB / 4;                 // 16-byte vectors per row
-                constexpr int RSTEP = T::THREADS / VPR;
-                const int vq = threadIdx.x % VPR, r0 = threadIdx.x / VPR;
-                const int kq = 4 * vq;
+                const int vq = threadIdx.x % VPR, kq = 4 * vq;
                 const int nb = max(0, min(16, 4 * (g.K - (kbase + kq))));
-                for (int r = r0; r < rows; r += RSTEP)
+                for (int r = threadIdx.x / VPR; r < rows; r += nthreads / VPR)
                     cp_async16(s_w + r * T::KB + kq, wsrc + (long long)r * g.K + (nb ? kq : 0), nb);
             } else {
-                for (int i = threadIdx.x; i < rows * T::KB; i += T::THREADS) {
+                for (int i = threadIdx.x; i < rows * T::KB; i += nthreads) {
                     const int kk = i % T::KB, r = i / T::KB;
                     const bool ok = kbase + kk < g.K;
                     cp_async4(s_w + i, wsrc + (long long)r * g.K + (ok ? kk : 0), ok ? 4 : 0);
@@ -382,10 +382,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
             cp_async_wait_all();
         }
         __syncthreads();
-        // ---- P1: window NZE lists, one warp per channel
-        for (int j = warp; j < chn; j += T::WARPS) {
+        // ---- P1: bucket every NZE of the strip's window columns into row-tile lists
+        for (int j = warp; j < chn; j += nwarps) {
             const int* seg = s_ptr + s_poff[j];
-            float4* lst = s_list + j * LCAP;
+            int* cnt = s_cnt + j * RT;
             ChanDir d;
             parse_channel_rel(g, seg, d);
             int lo = 0, hi = 0;
@@ -396,67 +396,70 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
             int* slo = spre + 32;
             spre[lane] = (lane < T::WW) ? pre : (1 << 30);
             slo[lane] = lo;
+            if (lane < RT) cnt[lane] = 0;
             const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
-            // contiguous when every window column starts where the flattened prefix says
             const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
             __syncwarp();
             const long long Z = s_z[j];
-            int cnt = 0;
-            // pass 1: load, keep rows of the tile window, compact {v, h, f}
-            for (int f0 = 0; f0 < tot; f0 += 128) {
-                int e[4], ff[4];
-                float v[4];
+            float4* lst = s_list + j * RT * T::LCAP;
+            constexpr int U = 2;
+            for (int f0 = 0; f0 < tot; f0 += 32 * U) {
+                int e[U], col[U];
+                float v[U];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < U; u++) {
                     const int f = f0 + 32 * u + lane;
-                    ff[u] = f;
                     e[u] = -1;
                     v[u] = 0.f;
+                    col[u] = 0;
                     if (f < tot) {
-                        int idx = lo0 + f;
-                        if (!contig) {
-                            int jc = 0;
+                        int jc = 0;
 #pragma unroll
-                            for (int step = 16; step > 0; step >>= 1)
-                                if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
-                            idx = slo[jc] + (f - spre[jc]);
-                        }
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                        col[u] = jc;
+                        const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
                         e[u] = __ldg(a.in + Z + idx);
                         v[u] = __ldg(a.da + Z + idx);
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int h = e[u] / T::S;     // IN = L + h*S with L < S
-                    const bool keep = e[u] >= 0 && h >= hy0 && h < hy0 + T::WH;
-                    const unsigned km = __ballot_sync(0xffffffffu, keep);
-                    if (keep)
-                        lst[cnt + __popc(km & lanemask_lt())] =
-                            make_float4(v[u], __int_as_float(h - hy0), __int_as_float(ff[u]), 0.f);
-                    cnt += __popc(km);
+                for (int u = 0; u < U; u++) {
+                    const int h = e[u] / T::S;                 // IN = L + h*S with L < S
+                    const bool ok = e[u] >= 0;
+                    // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h
+                    const int rhi = min(RT - 1, h / T::RSTEP);
+                    const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        const int r = rlo + q;
+                        const bool put = ok && r <= rhi;
+                        const unsigned pm = __ballot_sync(0xffffffffu, put);
+                        if (pm == 0) continue;
+                        const unsigned grp = __match_any_sync(0xffffffffu, put ? r : -1);
+                        int base = 0;
+                        const int leader = __ffs(grp) - 1;
+                        if (put && lane == leader) base = atomicAdd(cnt + r, __popc(grp));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        if (put) {
+                            const int pos = base + __popc(grp & lanemask_lt());
+                            lst[r * T::LCAP + pos] =
+                                make_float4(v[u], v[u], __int_as_float((h - r * T::RSTEP) * T::WW + col[u]), 0.f);
+                        }
+                    }
                 }
             }
             __syncwarp();
-            // pass 2: window column of each kept NZE -> replay entry {v, v, case, 0}
-            for (int i = lane; i < cnt; i += 32) {
-                const float4 t = lst[i];
-                const int f = __float_as_int(t.z);
-                int jc = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1)
-                    if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
-                lst[i] = make_float4(t.x, t.x, __int_as_float(__float_as_int(t.y) * T::WW + jc), 0.f);
-            }
-            if (lane == 0) {
-                lst[cnt] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
-                s_cnt[j] = cnt;
+            if (lane < RT) {   // close every row-tile list with the sentinel
+                float4* l = lst + lane * T::LCAP;
+                l[cnt[lane]] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
             }
             __syncwarp();
         }
         __syncthreads();
-        // ---- P2: FFMA replay (generated brx.idx jump table, FFMA2 bodies)
-        for (int j = cs; j < chn; j += T::CS) {
-            if (s_cnt[j] == 0) continue;
+        // ---- P2: FFMA replay of this warp's row tile (generated brx.idx / FFMA2 loop)
+        for (int j = cs; j < chn; j += CS) {
+            if (s_cnt[j * RT + rtile] == 0) continue;
             typename T::Word w[T::NP][T::R][T::S];
 #pragma unroll
             for (int p = 0; p < T::NP; p++)
@@ -466,24 +469,21 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
                     for (int m = 0; m < T::S; m++) {
                         const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane;
                         if constexpr (T::RP::kPacked) {
-                            const unsigned lo = __float_as_uint(ws[(kg * T::KPL + 2 * p) * 32]);
-                            const unsigned hi = __float_as_uint(ws[(kg * T::KPL + 2 * p + 1) * 32]);
+                            const unsigned lo = __float_as_uint(ws[(2 * p) * 32]);
+                            const unsigned hi = __float_as_uint(ws[(2 * p + 1) * 32]);
                             w[p][l][m] = (unsigned long long)lo | ((unsigned long long)hi << 32);
                         } else {
-                            w[p][l][m] = ws[(kg * T::KPL + p) * 32];
+                            w[p][l][m] = ws[p * 32];
                         }
                     }
-            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + j * LCAP), acc, w);
+            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + (j * RT + rtile) * T::LCAP), acc, w);
         }
         __syncthreads();
     }
 
-    // ---- epilogue 1: unpack, reduce the CS channel splits (all warps), CTA partial -> part
+    // ---- epilogue: unpack; reduce the csplit warps of each row tile; partial -> part
     constexpr int TT = T::TY * T::TX, TP = TT + 1;
-    constexpr int PIECE = 64 < T::NACC ? 64 : T::NACC;
-    float* red = s_w;                                              // [CS][KG][PIECE][32]
-    float* part = s_w + (T::CS > 1 ? T::CS * T::KG * PIECE * 32 : 0);   // [KG*KPL*32][TP]
-    float accf[T::NACC];
+    float accf[T::NACC];   // index kk*TT + t
 #pragma unroll
     for (int p = 0; p < T::NP; p++)
 #pragma unroll
@@ -495,43 +495,43 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) sparse_conv_kernel(ConvAr
                 accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
             }
         }
-    // accf index i = kk*TT + t  ->  part[((kg*KPL + kk)*32 + lane)*TP + t]
-    if constexpr (T::CS == 1) {
+    float* part = s_w;   // [RT][KB][TP]: row tile, output channel (kk*32 + lane), position
+    if (CS > 1) {
+        float* red = part + RT * T::KB * TP;   // [CS-1][RT][NACC][32]
+        if (cs > 0) {
 #pragma unroll
-        for (int i = 0; i < T::NACC; i++) part[((kg * T::KPL + i / TT) * 32 + lane) * TP + i % TT] = accf[i];
+            for (int i = 0; i < T::NACC; i++) red[(((cs - 1) * RT + rtile) * T::NACC + i) * 32 + lane] = accf[i];
+        }
+        __syncthreads();
+        if (cs == 0) {
+#pragma unroll
+            for (int i = 0; i < T::NACC; i++) {
+                float sum = accf[i];
+                for (int q = 1; q < CS; q++) sum += red[(((q - 1) * RT + rtile) * T::NACC + i) * 32 + lane];
+                part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = sum;
+            }
+        }
     } else {
 #pragma unroll
-        for (int pc = 0; pc < T::NACC / PIECE; pc++) {
-#pragma unroll
-            for (int i = 0; i < PIECE; i++) red[((cs * T::KG + kg) * PIECE + i) * 32 + lane] = accf[pc * PIECE + i];
-            __syncthreads();
-            constexpr int PER = PIECE / T::CS;
-            for (int i = cs * PER; i < (cs + 1) * PER; i++) {
-                float sum = 0.f;
-#pragma unroll
-                for (int q = 0; q < T::CS; q++) sum += red[((q * T::KG + kg) * PIECE + i) * 32 + lane];
-                const int gi = pc * PIECE + i;
-                part[((kg * T::KPL + gi / TT) * 32 + lane) * TP + gi % TT] = sum;
-            }
-            __syncthreads();
-        }
+        for (int i = 0; i < T::NACC; i++) part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = accf[i];
     }
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
-    // ---- epilogue 2: sum the cluster's partials (DSMEM), ReLU, store NKHW
+    // ---- sum the cluster's partials (DSMEM), ReLU, store NKHW
     float* peers[8];
 #pragma unroll
     for (int r = 0; r < 8; r++) peers[r] = (r < a.cg && r != rank) ? cgrp::this_cluster().map_shared_rank(part, r) : nullptr;
-    const int total = T::KB * TT;
+    const int total = RT * T::KB * TT;
     const int per = (total + a.cg - 1) / a.cg;
     const int i0 = rank * per, i1 = min(total, i0 + per);
-    for (int i = i0 + threadIdx.x; i < i1; i += T::THREADS) {
-        const int t = i % TT, kl = i / TT;        // kl = (kg*KPL + kk)*32 + lane
-        const int sidx = kl * TP + t;
+    for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
+        const int t = i % TT, rk = i / TT;        // rk = rtile*KB + kl
+        const int kl = rk % T::KB, rr = rk / T::KB;
+        const int sidx = rk * TP + t;
         float sum = part[sidx];
 #pragma unroll
         for (int r = 0; r < 8; r++)
             if (peers[r]) sum += peers[r][sidx];
-        const int k = kbase + kl, oy = oy0 + t / T::TX, ox = ox0 + t % T::TX;
+        const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + t % T::TX;
         if (k >= g.K || oy >= g.Oh || ox >= g.Ow) continue;
         if (a.relu) sum = fmaxf(sum, 0.f);
         a.y[(((long long)n * g.K + k) * g.Oh + oy) * g.Ow + ox] = sum;
@@ -597,37 +597,54 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
 }
 
 template <class T>
-static size_t tiled_smem(const ConvArgs& a) {
-    const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * (T::NCASE + 1) * 16 +
-                        (size_t)T::CH * a.pmax * 4 + (size_t)2 * T::CH * 4 + (size_t)(T::WARPS * 64 + 2) * 4 + 16 +
-                        (size_t)T::CH * 8;
-    constexpr int PIECE = 64 < T::NACC ? 64 : T::NACC;
-    const size_t red = (T::CS > 1 ? (size_t)T::CS * T::KG * PIECE * 32 * 4 : 0) +
-                       (size_t)T::KB * (T::TY * T::TX + 1) * 4;
-    return std::max(main, red);
+static size_t strip_smem(const ConvArgs& a) {
+    const int RT = a.rt, CS = a.csplit;
+    const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::LCAP * 16 +
+                        (size_t)T::CH * a.pmax * 4 + (size_t)T::CH * 4 + (size_t)T::CH * RT * 4 +
+                        (size_t)T::MAXW * 64 * 4 + 16 + (size_t)T::CH * 8;
+    const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX + 1) * 4 +
+                       (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
+    return std::max(main, epi);
+}
+
+// Channel split across a cluster: the largest cg in {1,2,4,8} that keeps the
+// grid within ~one wave of resident CTAs and at least 8 channels per CTA.
+static int pick_cg(long long ctas, int C, int per_sm) {
+    int best = 1;
+    for (int cg = 2; cg <= 8; cg *= 2)
+        if (ctas * cg <= 148LL * per_sm && C >= 8 * cg) best = cg;
+    return best;
+}
+
+// Development override: SPC_TUNE="<cg>" forces the cluster split.
+static int tune_cg() {
+    static const char* env = getenv("SPC_TUNE");
+    return env ? atoi(env) : 0;
 }
 
 template <class T>
-static cudaError_t run_tiled(ConvArgs& a, int cg, cudaStream_t st) {
+static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
-    const int tx = (g.Ow + T::TX - 1) / T::TX, ty = (g.Oh + T::TY - 1) / T::TY;
-    a.tiles_x = tx;
-    a.cg = cg;
+    const int strips = (g.Ow + T::TX - 1) / T::TX;
+    a.rt = (g.Oh + T::TY - 1) / T::TY;
+    if (a.rt > T::MAXW) return cudaErrorInvalidValue;
+    a.csplit = std::max(1, T::MAXW / a.rt);
     const int kblocks = (g.K + T::KB - 1) / T::KB;
-    const size_t smem = tiled_smem<T>(a);
+    const long long ctas = (long long)strips * kblocks * g.N;
+    int cg = tune_cg();
+    if (cg <= 0) cg = pick_cg(ctas, g.C, T::MINB);
+    a.cg = cg;
+    const size_t smem = strip_smem<T>(a);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static bool attr_set = false;     // per instantiation
-    static size_t attr_bytes = 0;
-    if (!attr_set || attr_bytes < smem) {
-        cudaError_t err = cudaFuncSetAttribute(sparse_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)std::max(smem, attr_bytes));
+    static size_t attr_bytes = 0;     // per instantiation
+    if (attr_bytes < smem) {
+        cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
-        attr_set = true;
-        attr_bytes = std::max(smem, attr_bytes);
+        attr_bytes = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(tx * ty, kblocks, g.N * cg);
-    cfg.blockDim = dim3(T::THREADS);
+    cfg.gridDim = dim3(strips, kblocks, g.N * cg);
+    cfg.blockDim = dim3(32 * a.rt * a.csplit);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -637,40 +654,7 @@ static cudaError_t run_tiled(ConvArgs& a, int cg, cudaStream_t st) {
     attr[0].val.clusterDim.z = cg;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, sparse_conv_kernel<T>, a);
-}
-
-// Channel split across a cluster: the largest cg in {1,2,3,4,6,8} that keeps the
-// grid within one wave of resident CTAs and at least 8 channels per CTA.
-static int pick_cg(long long ctas, int C, int minb) {
-    int best = 1;
-    const int cands[] = {1, 2, 3, 4, 6, 8};
-    for (int cg : cands)
-        if (ctas * cg <= 148LL * minb && C >= 8 * cg) best = cg;
-    return best;
-}
-
-// Development override: SPC_TUNE="<config>:<cg>" (cg 0 = automatic).
-static const char* tune_cfg(int* cg) {
-    static const char* env = getenv("SPC_TUNE");
-    *cg = 0;
-    if (!env) return nullptr;
-    const char* colon = strchr(env, ':');
-    if (colon) *cg = atoi(colon + 1);
-    return env;
-}
-
-template <class T>
-static cudaError_t run_auto(ConvArgs& a, int cg_override, cudaStream_t st) {
-    const Geom& g = a.g;
-    const long long ctas = (long long)((g.Oh + T::TY - 1) / T::TY) * ((g.Ow + T::TX - 1) / T::TX) *
-                           ((g.K + T::KB - 1) / T::KB) * g.N;
-    const int cg = cg_override > 0 ? cg_override : pick_cg(ctas, g.C, T::MINB);
-    return run_tiled<T>(a, cg, st);
-}
-
-static bool tune_is(const char* t, const char* name) {
-    return t && strncmp(t, name, strlen(name)) == 0 && (t[strlen(name)] == ':' || t[strlen(name)] == 0);
+    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T>, a);
 }
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
@@ -687,50 +671,31 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.relu = relu;
     a.tiles_x = 1;
     a.cg = 1;
+    a.rt = 1;
+    a.csplit = 1;
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
-    int tcg = 0;
-    const char* t = tune_cfg(&tcg);
+    cudaError_t err = cudaErrorNotSupported;
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        using A = TileCfg<3, 3, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
-        using B = TileCfg<3, 3, 1, 1, 4, 8, 2, 1, 8, 16, 2>;
-        using C = TileCfg<3, 3, 1, 1, 4, 8, 2, 1, 4, 16, 3>;
-        using D = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 8, 16, 1>;
-        using E = TileCfg<3, 3, 1, 1, 4, 8, 4, 1, 4, 16, 2>;
-        using F = TileCfg<3, 3, 1, 1, 8, 8, 1, 1, 8, 16, 1>;
-        if (tune_is(t, "A")) return run_auto<A>(a, tcg, st);
-        if (tune_is(t, "B")) return run_auto<B>(a, tcg, st);
-        if (tune_is(t, "C")) return run_auto<C>(a, tcg, st);
-        if (tune_is(t, "D")) return run_auto<D>(a, tcg, st);
-        if (tune_is(t, "E")) return run_auto<E>(a, tcg, st);
-        if (g.K <= 32) return run_auto<F>(a, tcg, st);
-        if (g.K <= 64) return run_auto<B>(a, tcg, st);
-        return run_auto<E>(a, tcg, st);
+        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1>>(a, st);
+        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2>>(a, st);
+        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 1, 1, 4, 4, 4>>(a, st);
+        else if (g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 4, 1>>(a, st);
+    } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
+        if (g.K <= 64 && g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 2>>(a, st);
+        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4>>(a, st);
+    } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
+        err = run_strip<StripCfg<1, 7, 1, 1, 8, 4, 2>>(a, st);
+    } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
+        err = run_strip<StripCfg<7, 1, 1, 1, 8, 4, 2>>(a, st);
     }
-    if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
-        using A = TileCfg<3, 3, 2, 2, 4, 8, 2, 1, 8, 16, 2>;
-        using B = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 8, 16, 1>;
-        using C = TileCfg<3, 3, 2, 2, 4, 8, 4, 1, 4, 16, 2>;
-        if (tune_is(t, "A")) return run_auto<A>(a, tcg, st);
-        if (tune_is(t, "B")) return run_auto<B>(a, tcg, st);
-        if (tune_is(t, "C")) return run_auto<C>(a, tcg, st);
-        if (g.K <= 64) return run_auto<A>(a, tcg, st);
-        return run_auto<C>(a, tcg, st);
-    }
-    if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1) {
-        using A = TileCfg<1, 7, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
-        return run_auto<A>(a, tcg, st);
-    }
-    if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1) {
-        using A = TileCfg<7, 1, 1, 1, 8, 8, 2, 1, 8, 16, 1>;
-        return run_auto<A>(a, tcg, st);
-    }
+    if (err != cudaErrorNotSupported) return err;
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
     if (WW > 32) return cudaErrorInvalidValue;
     a.tiles_x = (g.Ow + kGenTX - 1) / kGenTX;
     const int ty = (g.Oh + kGenTY - 1) / kGenTY;
     size_t smem = (size_t)kGenWarps * kGenTY * kGenTX * 32 * sizeof(float) + (size_t)kGenWarps * WH * WW * sizeof(float2);
-    cudaError_t err = cudaFuncSetAttribute(sparse_conv_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    err = cudaFuncSetAttribute(sparse_conv_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     dim3 grid(a.tiles_x * ty, (g.K + 31) / 32, g.N);
     sparse_conv_generic_kernel<<<grid, kGenWarps * 32, smem, st>>>(a, WH, WW);

@@ -16,9 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SETTINGS = {
-    "s1": ["auto", "A", "A:1", "A:2", "A:4", "B", "B:1", "B:2", "B:4", "C", "C:2", "C:4", "D", "D:2", "E", "E:2", "E:4"],
-    "s2": ["auto", "A", "A:2", "B", "B:2", "C", "C:2", "C:4"],
-    "x7": ["auto"],
+    "s1": ["auto", "1", "2", "4", "8"],
+    "s2": ["auto", "1", "2", "4"],
+    "x7": ["auto", "1", "2"],
 }
 WORKLOADS = {"cfg2": "s1", "cfg3": "s1", "cfg3s2": "s2", "cfg5L0": "s1", "cfg5L8": "s1", "cfg5L14": "s1",
              "cfg5L3": "s2", "cfg5L12": "s2", "cfg4a": "x7", "cfg4b": "x7", "cfg1": "s1"}
