@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             int* slo = spre + 32;
             spre[lane] = (lane < T::WW) ? pre : (1 << 30);
             slo[lane] = lo;
-            if (lane < RT) cnt[lane] = 0;
+            int my_cnt = 0;   // lane r < RT counts the entries of row tile r
             const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
             const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
             __syncwarp();
@@ -427,32 +427,30 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 for (int u = 0; u < U; u++) {
                     const int h = e[u] / T::S;                 // IN = L + h*S with L < S
                     const bool ok = e[u] >= 0;
-                    // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h
+                    // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
                     const int rhi = min(RT - 1, h / T::RSTEP);
                     const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
 #pragma unroll
                     for (int q = 0; q < 2; q++) {
                         const int r = rlo + q;
                         const bool put = ok && r <= rhi;
-                        const unsigned pm = __ballot_sync(0xffffffffu, put);
-                        if (pm == 0) continue;
-                        const unsigned grp = __match_any_sync(0xffffffffu, put ? r : -1);
-                        int base = 0;
-                        const int leader = __ffs(grp) - 1;
-                        if (put && lane == leader) base = atomicAdd(cnt + r, __popc(grp));
-                        base = __shfl_sync(0xffffffffu, base, leader);
-                        if (put) {
-                            const int pos = base + __popc(grp & lanemask_lt());
-                            lst[r * T::LCAP + pos] =
-                                make_float4(v[u], v[u], __int_as_float((h - r * T::RSTEP) * T::WW + col[u]), 0.f);
+                        unsigned pm = __ballot_sync(0xffffffffu, put);
+                        while (pm) {   // one round per distinct row tile in this chunk (usually 1-2)
+                            const int rr = __shfl_sync(0xffffffffu, r, __ffs(pm) - 1);
+                            const unsigned m = __ballot_sync(0xffffffffu, put && r == rr);
+                            const int base = __shfl_sync(0xffffffffu, my_cnt, rr);
+                            if (put && r == rr)
+                                lst[rr * T::LCAP + base + __popc(m & lanemask_lt())] =
+                                    make_float4(v[u], v[u], __int_as_float((h - rr * T::RSTEP) * T::WW + col[u]), 0.f);
+                            if (lane == rr) my_cnt += __popc(m);
+                            pm &= ~m;
                         }
                     }
                 }
             }
-            __syncwarp();
             if (lane < RT) {   // close every row-tile list with the sentinel
-                float4* l = lst + lane * T::LCAP;
-                l[cnt[lane]] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
+                lst[lane * T::LCAP + my_cnt] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
+                cnt[lane] = my_cnt;
             }
             __syncwarp();
         }
@@ -516,27 +514,33 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         for (int i = 0; i < T::NACC; i++) part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = accf[i];
     }
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
-    // ---- sum the cluster's partials (DSMEM), ReLU, store NKHW
-    float* peers[8];
-#pragma unroll
-    for (int r = 0; r < 8; r++) peers[r] = (r < a.cg && r != rank) ? cgrp::this_cluster().map_shared_rank(part, r) : nullptr;
+    // ---- sum the cluster's partials (DSMEM), ReLU, store NKHW (t = ty*TX + tx fastest)
+    static_assert((TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "power-of-two tile and k block");
     const int total = RT * T::KB * TT;
     const int per = (total + a.cg - 1) / a.cg;
     const int i0 = rank * per, i1 = min(total, i0 + per);
-    for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
-        const int t = i % TT, rk = i / TT;        // rk = rtile*KB + kl
-        const int kl = rk % T::KB, rr = rk / T::KB;
-        const int sidx = rk * TP + t;
-        float sum = part[sidx];
+    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
+    if (a.cg == 1) {
+        for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
+            const int t = i & (TT - 1), rk = i / TT, kl = rk & (T::KB - 1), rr = rk / T::KB;
+            const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + (t & (T::TX - 1));
+            float sum = part[rk * TP + t];
+            if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
+        }
+    } else {
+        float* peers[8];
 #pragma unroll
-        for (int r = 0; r < 8; r++)
-            if (peers[r]) sum += peers[r][sidx];
-        const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + t % T::TX;
-        if (k >= g.K || oy >= g.Oh || ox >= g.Ow) continue;
-        if (a.relu) sum = fmaxf(sum, 0.f);
-        a.y[(((long long)n * g.K + k) * g.Oh + oy) * g.Ow + ox] = sum;
+        for (int r = 0; r < 8; r++) peers[r] = (r < a.cg) ? cgrp::this_cluster().map_shared_rank(part, r) : nullptr;
+        for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
+            const int t = i & (TT - 1), rk = i / TT, kl = rk & (T::KB - 1), rr = rk / T::KB;
+            const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + (t & (T::TX - 1));
+            const int sidx = rk * TP + t;
+            float sum = 0.f;
+            for (int r = 0; r < a.cg; r++) sum += peers[r][sidx];
+            if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
+        }
+        cgrp::this_cluster().sync();
     }
-    if (a.cg > 1) cgrp::this_cluster().sync();
 }
 
 // Generic variant: any R, S, stride; TY x TX = 4 x 4 tile, accumulators in smem.

@@ -48,43 +48,49 @@ def gen(R, S, SH, SW, TY, TX, KPL):
     lines = []
     a = lines.append
     a("{")
-    a(".reg .b32 %%spcP, %%spcC, %%spcN0, %%spcN1, %%spcNC, %%spcNX;")
-    a(".reg .b64 %%spcVV;" if packed else ".reg .f32 %%spcF;")
+    # Two register sets A / B hold consecutive list entries; the case bodies
+    # exist twice (tables A and B).  A body of set X runs the FFMA2s with X's
+    # value, then reloads X with the entry two positions ahead and dispatches
+    # on the other set's case, which was loaded one full body earlier -- the
+    # shared-memory and jump-table latencies overlap the FFMA2s and no register
+    # rotation is needed.  Entries are 16 bytes {v, v, case, 0}: the value pair
+    # is one 64-bit register (FFMA2 operand); the list ends with a sentinel
+    # (case NCASE -> $Ldone) followed by one padding entry.
+    a(".reg .b32 %%spcP, %%spcAC, %%spcBC;")
+    a(".reg .b64 %%spcAV, %%spcBV, %%spcAX, %%spcBX;")
+    if not packed:
+        a(".reg .b32 %%spcAF, %%spcBF, %%spcAH, %%spcBH;")
     a(f"mov.b32 %%spcP, %{o_list};")
-    # list entries are 16 bytes {v, v, case, 0}, closed by a sentinel entry whose
-    # case is NCASE (-> $Ldone) and one padding entry (read by the prefetch).
-    # Software pipeline: while the body of entry i runs, entry i+1 is already in
-    # registers (N*) and entry i+2 is being loaded.
-    a("ld.shared.v4.b32 {%%spcN0, %%spcN1, %%spcNC, %%spcNX}, [%%spcP];")
-    a("add.u32 %%spcP, %%spcP, 16;")
-    def dispatch():
-        if packed:
-            a("mov.b64 %%spcVV, {%%spcN0, %%spcN1};")
-        else:
-            a("mov.b32 %%spcF, %%spcN0;")
-        a("mov.b32 %%spcC, %%spcNC;")
-        a("ld.shared.v4.b32 {%%spcN0, %%spcN1, %%spcNC, %%spcNX}, [%%spcP];")
-        a("add.u32 %%spcP, %%spcP, 16;")
-        a("brx.idx.uni %%spcC, $Ltab%=;")
+    a("ld.shared.v2.b64 {%%spcAV, %%spcAX}, [%%spcP];")
+    a("ld.shared.v2.b64 {%%spcBV, %%spcBX}, [%%spcP+16];")
+    a("add.u32 %%spcP, %%spcP, 32;")
     ncase = WH * WW
-    a("$Ltab%=: .branchtargets " + ", ".join(f"$Lc{c}%=" for c in range(ncase)) + ", $Ldone%=;")
-    dispatch()
-    for c in range(ncase):
-        hr, wr = divmod(c, WW)
-        a(f"$Lc{c}%=:")
-        for l in range(R):
-            for m in range(S):
-                y1, x1 = hr - l, wr - m
-                if y1 < 0 or x1 < 0 or y1 % SH or x1 % SW or y1 // SH >= TY or x1 // SW >= TX:
-                    continue
-                y, x = y1 // SH, x1 // SW
-                for p in range(NP):
-                    ai, wi = acc(p, y, x), wop(p, l, m)
-                    if packed:
-                        a(f"fma.rn.f32x2 %{ai}, %%spcVV, %{wi}, %{ai};")
-                    else:
-                        a(f"fma.rn.f32 %{ai}, %%spcF, %{wi}, %{ai};")
-        dispatch()
+    for X, Y in (("A", "B"), ("B", "A")):
+        a(f"$Ltab{X}%=: .branchtargets " + ", ".join(f"$L{X}{c}%=" for c in range(ncase)) + ", $Ldone%=;")
+    a("cvt.u32.u64 %%spcAC, %%spcAX;")
+    a("brx.idx.uni %%spcAC, $LtabA%=;")
+    for X, Y in (("A", "B"), ("B", "A")):
+        for c in range(ncase):
+            hr, wr = divmod(c, WW)
+            a(f"$L{X}{c}%=:")
+            a(f"cvt.u32.u64 %%spc{Y}C, %%spc{Y}X;")
+            if not packed:
+                a(f"mov.b64 {{%%spc{X}F, %%spc{X}H}}, %%spc{X}V;")
+            for l in range(R):
+                for m in range(S):
+                    y1, x1 = hr - l, wr - m
+                    if y1 < 0 or x1 < 0 or y1 % SH or x1 % SW or y1 // SH >= TY or x1 // SW >= TX:
+                        continue
+                    y, x = y1 // SH, x1 // SW
+                    for p in range(NP):
+                        ai, wi = acc(p, y, x), wop(p, l, m)
+                        if packed:
+                            a(f"fma.rn.f32x2 %{ai}, %%spc{X}V, %{wi}, %{ai};")
+                        else:
+                            a(f"fma.rn.f32 %{ai}, %%spc{X}F, %{wi}, %{ai};")
+            a(f"ld.shared.v2.b64 {{%%spc{X}V, %%spc{X}X}}, [%%spcP];")
+            a("add.u32 %%spcP, %%spcP, 16;")
+            a(f"brx.idx.uni %%spc{Y}C, $Ltab{Y}%=;")
     a("$Ldone%=:")
     a("}")
     asm = "\n".join('        "' + ln + '\\n"' for ln in lines)
@@ -105,7 +111,7 @@ __device__ __forceinline__ void {name}(unsigned list_smem, {T} (&acc)[{NP}][{TY}
 template <> struct Replay<{R}, {S}, {SH}, {SW}, {TY}, {TX}, {KPL}> {{
     static constexpr bool kPacked = {str(packed).lower()};
     using Word = {T};
-    static constexpr int kSentinel = {ncase};
+    static constexpr int kSentinel = {ncase};  // lists: entries, sentinel, 1 padding entry
     __device__ __forceinline__ static void run(unsigned list_smem, {T} (&acc)[{NP}][{TY}][{TX}],
                                                const {T} (&w)[{NP}][{R}][{S}]) {{
         {name}(list_smem, acc, w);
