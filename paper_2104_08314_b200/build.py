@@ -26,18 +26,11 @@ def stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + \
-        [os.path.join(HERE, "..", "include", "spconv.h"), os.path.join(HERE, "..", "tools", "gen_dispatch.py")]
+        [os.path.join(HERE, "..", "include", "spconv.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def generate() -> None:
-    """Regenerate csrc/dispatch_gen.cuh (inline-PTX replay loops)."""
-    subprocess.check_call([sys.executable, os.path.join(HERE, "..", "tools", "gen_dispatch.py")],
-                          stdout=subprocess.DEVNULL)
-
-
 def build(force: bool = False, verbose: bool = False) -> str:
-    generate()
     if not force and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

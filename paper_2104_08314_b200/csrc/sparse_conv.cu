@@ -22,13 +22,13 @@
 //  * the GENERIC variant (any R, S, stride) runs the same pipeline with smem
 //    accumulators and runtime tap loops.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
 #include <cooperative_groups.h>
 
 #include "common.cuh"
-#include "dispatch_gen.cuh"
 
 namespace spc {
 
@@ -232,7 +232,7 @@ struct ConvArgs {
 
 // Strip-kernel configuration: a CTA owns a column strip of TX output columns and
 // all output rows (rt row tiles of TY rows, one per warp), KPL output channels
-// per lane (pairs (k, k+32) packed for FFMA2 when KPL is even), CH input
+// per lane (pairs (k, k+32) as float2 for FFMA2 when KPL is even), CH input
 // channels staged per chunk.
 template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2>
 struct StripCfg {
@@ -244,13 +244,14 @@ struct StripCfg {
     static constexpr int NACC = KPL * TY * TX;        // accumulators per lane
     static constexpr int WH = (TY - 1) * SH + R;      // input window rows of a row tile
     static constexpr int WW = (TX - 1) * SW + S;      // input window cols of the strip
-    static constexpr int NCASE = WH * WW;
-    static constexpr int LCAP = NCASE + 2;            // list slots: entries + sentinel + prefetch pad
+    static constexpr int NCASE = WH * WW;             // window positions
+    static constexpr int MW = (NCASE + 31) / 32;      // 32-bit occupancy words per window
+    static constexpr int NCP = 32 * MW;               // dense window slots (floats)
     static constexpr int RSTEP = TY * SH;             // input rows between row tiles
+    static constexpr bool PACKED = (KPL % 2) == 0;
+    static constexpr int NP = PACKED ? KPL / 2 : KPL; // accumulator words per position
     static_assert(WW <= 32, "window columns are mapped to lanes");
-    using RP = Replay<R, S, SH, SW, TY, TX, KPL>;
-    using Word = typename RP::Word;
-    static constexpr int NP = RP::kPacked ? KPL / 2 : KPL;
+    static_assert(MW <= 4, "window too large");
 };
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
@@ -303,6 +304,46 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg,
     return n;
 }
 
+// One window position P of the replay: the NZE value v (already known to be
+// non-zero) times each tap (l, m) whose output (y, x) lies in the row tile and
+// on the stride grid; all indices are compile-time constants after unrolling.
+template <class T>
+__device__ __forceinline__ void tap_fma(int P, float v, float2 (&acc)[T::NP][T::TY][T::TX],
+                                        const float2 (&w)[T::NP][T::R][T::S]) {
+    const int hr = P / T::WW, wr = P % T::WW;
+    const float2 vv = make_float2(v, v);
+#pragma unroll
+    for (int l = 0; l < T::R; ++l)
+#pragma unroll
+        for (int m = 0; m < T::S; ++m) {
+            const int y1 = hr - l, x1 = wr - m;
+            if (y1 >= 0 && x1 >= 0 && (y1 % T::SH) == 0 && (x1 % T::SW) == 0 && y1 / T::SH < T::TY &&
+                x1 / T::SW < T::TX) {
+#pragma unroll
+                for (int p = 0; p < T::NP; ++p)
+                    acc[p][y1 / T::SH][x1 / T::SW] = __ffma2_rn(vv, w[p][l][m], acc[p][y1 / T::SH][x1 / T::SW]);
+            }
+        }
+}
+
+template <class T>
+__device__ __forceinline__ void tap_fma1(int P, float v, float (&acc)[T::NP][T::TY][T::TX],
+                                         const float (&w)[T::NP][T::R][T::S]) {
+    const int hr = P / T::WW, wr = P % T::WW;
+#pragma unroll
+    for (int l = 0; l < T::R; ++l)
+#pragma unroll
+        for (int m = 0; m < T::S; ++m) {
+            const int y1 = hr - l, x1 = wr - m;
+            if (y1 >= 0 && x1 >= 0 && (y1 % T::SH) == 0 && (x1 % T::SW) == 0 && y1 / T::SH < T::TY &&
+                x1 / T::SW < T::TX) {
+#pragma unroll
+                for (int p = 0; p < T::NP; ++p)
+                    acc[p][y1 / T::SH][x1 / T::SW] = fmaf(v, w[p][l][m], acc[p][y1 / T::SH][x1 / T::SW]);
+            }
+        }
+}
+
 // Strip kernel.  CTA = (image n, column strip of TX outputs, KB output
 // channels, input-channel range of its cluster rank); warp (r, cs) owns row
 // tile r of the strip for the channels cs, cs+csplit, ...  Per chunk of CH
@@ -311,10 +352,12 @@ __device__ __forceinline__ int build_list(const ConvArgs& a, const int32_t* seg,
 //      taps W[c][l][m][kbase..+KB) in shared memory (cp.async);
 //  P1  one warp per channel: block directory from the staged ptr (NPC / NPF skip),
 //      DA ranges of the strip's window columns, then every NZE of those columns
-//      (many loads in flight) is bucketed into the list of each row tile whose
-//      window holds it (1 or 2), as a replay entry {v, v, window position, 0};
-//  P2  warp (r, cs) replays its lists (generated brx.idx / FFMA2 loop) into
-//      register accumulators.
+//      (many loads in flight) is scattered into the dense window array of each
+//      row tile whose window holds it (1 or 2 tiles);
+//  P2  warp (r, cs), per channel: occupancy mask of its window (2 ballots), then
+//      a fully unrolled walk over the window positions: a warp-uniform skip
+//      branch for empty positions, static FFMA2 taps for the NZEs.  Only NZEs
+//      cost multiply-adds (Alg. 2 convSpMv), with no indirect branches.
 // Epilogue: reduce the csplit warps of a row tile through smem, then the cg
 // CTAs of the cluster through distributed shared memory; ReLU; NKHW store.
 template <class T>
@@ -334,27 +377,30 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
-    float4* s_list = reinterpret_cast<float4*>(s_w + T::CH * T::RS * T::KB);          // [CH][RT][LCAP]
-    int* s_ptr = reinterpret_cast<int*>(s_list + T::CH * RT * T::LCAP);               // [CH * pmax]
+    float* s_val = s_w + T::CH * T::RS * T::KB;                                       // [CH][RT][NCP]
+    int* s_ptr = reinterpret_cast<int*>(s_val + T::CH * RT * T::NCP);                 // [CH * pmax]
     int* s_poff = s_ptr + T::CH * a.pmax;                                             // [CH]
-    int* s_cnt = s_poff + T::CH;                                                      // [CH][RT]
-    int* s_scr = s_cnt + T::CH * RT;                                                  // [MAXW][64]
+    int* s_scr = s_poff + T::CH;                                                      // [MAXW][64]
     long long* s_z = reinterpret_cast<long long*>(
         (reinterpret_cast<uintptr_t>(s_scr + T::MAXW * 64) + 7) & ~uintptr_t(7));      // [CH]
 
-    typename T::Word acc[T::NP][T::TY][T::TX];
+    using AccT = typename std::conditional<T::PACKED, float2, float>::type;
+    AccT acc[T::NP][T::TY][T::TX];
 #pragma unroll
     for (int p = 0; p < T::NP; p++)
 #pragma unroll
         for (int yy = 0; yy < T::TY; yy++)
 #pragma unroll
-            for (int xx = 0; xx < T::TX; xx++) acc[p][yy][xx] = 0;
+            for (int xx = 0; xx < T::TX; xx++) {
+                if constexpr (T::PACKED) acc[p][yy][xx] = make_float2(0.f, 0.f);
+                else acc[p][yy][xx] = 0.f;
+            }
     const bool w16 = (g.K % 4) == 0;
 
     for (int c0 = c_begin; c0 < c_end; c0 += T::CH) {
         const int chn = min(T::CH, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
-        // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight)
+        // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight); zero the windows
         {
             const long long pbase = __ldg(a.cpo_off + nc0);
             const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
@@ -379,30 +425,31 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     cp_async4(s_w + i, wsrc + (long long)r * g.K + (ok ? kk : 0), ok ? 4 : 0);
                 }
             }
+            float4* v4 = reinterpret_cast<float4*>(s_val);
+            for (int i = threadIdx.x; i < chn * RT * T::NCP / 4; i += nthreads) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             cp_async_wait_all();
         }
         __syncthreads();
-        // ---- P1: bucket every NZE of the strip's window columns into row-tile lists
+        // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
         for (int j = warp; j < chn; j += nwarps) {
             const int* seg = s_ptr + s_poff[j];
-            int* cnt = s_cnt + j * RT;
             ChanDir d;
             parse_channel_rel(g, seg, d);
+            if (d.npc) continue;                                  // NPC: skip channel
             int lo = 0, hi = 0;
-            if (!d.npc && lane < T::WW) column_range_rel(g, seg, d, wx0 + lane, lo, hi);
+            if (lane < T::WW) column_range_rel(g, seg, d, wx0 + lane, lo, hi);
             int tot;
             const int pre = warp_exclusive_scan(hi - lo, &tot);
             int* spre = s_scr + warp * 64;
             int* slo = spre + 32;
             spre[lane] = (lane < T::WW) ? pre : (1 << 30);
             slo[lane] = lo;
-            int my_cnt = 0;   // lane r < RT counts the entries of row tile r
             const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
             const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
             __syncwarp();
             const long long Z = s_z[j];
-            float4* lst = s_list + j * RT * T::LCAP;
-            constexpr int U = 2;
+            float* win = s_val + j * RT * T::NCP;
+            constexpr int U = 4;
             for (int f0 = 0; f0 < tot; f0 += 32 * U) {
                 int e[U], col[U];
                 float v[U];
@@ -425,40 +472,29 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
+                    if (e[u] < 0) continue;
                     const int h = e[u] / T::S;                 // IN = L + h*S with L < S
-                    const bool ok = e[u] >= 0;
                     // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
                     const int rhi = min(RT - 1, h / T::RSTEP);
                     const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
-#pragma unroll
-                    for (int q = 0; q < 2; q++) {
-                        const int r = rlo + q;
-                        const bool put = ok && r <= rhi;
-                        unsigned pm = __ballot_sync(0xffffffffu, put);
-                        while (pm) {   // one round per distinct row tile in this chunk (usually 1-2)
-                            const int rr = __shfl_sync(0xffffffffu, r, __ffs(pm) - 1);
-                            const unsigned m = __ballot_sync(0xffffffffu, put && r == rr);
-                            const int base = __shfl_sync(0xffffffffu, my_cnt, rr);
-                            if (put && r == rr)
-                                lst[rr * T::LCAP + base + __popc(m & lanemask_lt())] =
-                                    make_float4(v[u], v[u], __int_as_float((h - rr * T::RSTEP) * T::WW + col[u]), 0.f);
-                            if (lane == rr) my_cnt += __popc(m);
-                            pm &= ~m;
-                        }
-                    }
+                    for (int r = rlo; r <= rhi; r++) win[r * T::NCP + (h - r * T::RSTEP) * T::WW + col[u]] = v[u];
                 }
             }
-            if (lane < RT) {   // close every row-tile list with the sentinel
-                lst[lane * T::LCAP + my_cnt] = make_float4(0.f, 0.f, __int_as_float(T::RP::kSentinel), 0.f);
-                cnt[lane] = my_cnt;
-            }
-            __syncwarp();
         }
         __syncthreads();
-        // ---- P2: FFMA replay of this warp's row tile (generated brx.idx / FFMA2 loop)
+        // ---- P2: unrolled walk over the window positions of this warp's row tile
         for (int j = cs; j < chn; j += CS) {
-            if (s_cnt[j * RT + rtile] == 0) continue;
-            typename T::Word w[T::NP][T::R][T::S];
+            const float* win = s_val + (j * RT + rtile) * T::NCP;
+            unsigned mw[T::MW];
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < T::MW; q++) {
+                mw[q] = __ballot_sync(0xffffffffu, win[32 * q + lane] != 0.0f);
+                any |= mw[q] != 0;
+            }
+            if (!any) continue;
+            using WT = typename std::conditional<T::PACKED, float2, float>::type;
+            WT w[T::NP][T::R][T::S];
 #pragma unroll
             for (int p = 0; p < T::NP; p++)
 #pragma unroll
@@ -466,29 +502,37 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 #pragma unroll
                     for (int m = 0; m < T::S; m++) {
                         const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane;
-                        if constexpr (T::RP::kPacked) {
-                            const unsigned lo = __float_as_uint(ws[(2 * p) * 32]);
-                            const unsigned hi = __float_as_uint(ws[(2 * p + 1) * 32]);
-                            w[p][l][m] = (unsigned long long)lo | ((unsigned long long)hi << 32);
-                        } else {
-                            w[p][l][m] = ws[p * 32];
-                        }
+                        if constexpr (T::PACKED) w[p][l][m] = make_float2(ws[(2 * p) * 32], ws[(2 * p + 1) * 32]);
+                        else w[p][l][m] = ws[p * 32];
                     }
-            T::RP::run((unsigned)__cvta_generic_to_shared(s_list + (j * RT + rtile) * T::LCAP), acc, w);
+            const float4* w4 = reinterpret_cast<const float4*>(win);
+#pragma unroll
+            for (int q4 = 0; q4 < (T::NCASE + 3) / 4; q4++) {
+                const float4 vq = w4[q4];
+                const float vv[4] = {vq.x, vq.y, vq.z, vq.w};
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int P = 4 * q4 + u;
+                    if (P < T::NCASE && ((mw[P >> 5] >> (P & 31)) & 1u)) {
+                        if constexpr (T::PACKED) tap_fma<T>(P, vv[u], acc, w);
+                        else tap_fma1<T>(P, vv[u], acc, w);
+                    }
+                }
+            }
         }
         __syncthreads();
     }
 
-    // ---- epilogue: unpack; reduce the csplit warps of each row tile; partial -> part
+    // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
     constexpr int TT = T::TY * T::TX, TP = TT + 1;
     float accf[T::NACC];   // index kk*TT + t
 #pragma unroll
     for (int p = 0; p < T::NP; p++)
 #pragma unroll
         for (int t = 0; t < TT; t++) {
-            if constexpr (T::RP::kPacked) {
-                accf[(2 * p) * TT + t] = __uint_as_float((unsigned)(acc[p][t / T::TX][t % T::TX] & 0xffffffffull));
-                accf[(2 * p + 1) * TT + t] = __uint_as_float((unsigned)(acc[p][t / T::TX][t % T::TX] >> 32));
+            if constexpr (T::PACKED) {
+                accf[(2 * p) * TT + t] = acc[p][t / T::TX][t % T::TX].x;
+                accf[(2 * p + 1) * TT + t] = acc[p][t / T::TX][t % T::TX].y;
             } else {
                 accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
             }
@@ -603,9 +647,9 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
 template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
-    const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::LCAP * 16 +
-                        (size_t)T::CH * a.pmax * 4 + (size_t)T::CH * 4 + (size_t)T::CH * RT * 4 +
-                        (size_t)T::MAXW * 64 * 4 + 16 + (size_t)T::CH * 8;
+    const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
+                        (size_t)T::CH * a.pmax * 4 + (size_t)T::CH * 4 + (size_t)T::MAXW * 64 * 4 + 16 +
+                        (size_t)T::CH * 8;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX + 1) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
