@@ -249,6 +249,7 @@ struct StripCfg {
     static constexpr int NCP = 32 * MW;               // dense window slots (floats)
     static constexpr int RSTEP = TY * SH;             // input rows between row tiles
     static constexpr bool PACKED = (KPL % 2) == 0;
+    static constexpr int GBH = 4, GBW = 2;            // skip-branch block of window positions
     static constexpr int NP = PACKED ? KPL / 2 : KPL; // accumulator words per position
     static_assert(WW <= 32, "window columns are mapped to lanes");
     static_assert(MW <= 4, "window too large");
@@ -505,20 +506,41 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                         if constexpr (T::PACKED) w[p][l][m] = make_float2(ws[(2 * p) * 32], ws[(2 * p + 1) * 32]);
                         else w[p][l][m] = ws[p * 32];
                     }
-            const float4* w4 = reinterpret_cast<const float4*>(win);
+            // blocks of GBH x GBW window positions: one warp-uniform skip branch per
+            // block (a body of ~8 positions x taps keeps ptxas from if-converting it),
+            // per-position predication inside the block
 #pragma unroll
-            for (int q4 = 0; q4 < (T::NCASE + 3) / 4; q4++) {
-                const float4 vq = w4[q4];
-                const float vv[4] = {vq.x, vq.y, vq.z, vq.w};
+            for (int by = 0; by < T::WH; by += T::GBH)
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int P = 4 * q4 + u;
-                    if (P < T::NCASE && ((mw[P >> 5] >> (P & 31)) & 1u)) {
-                        if constexpr (T::PACKED) tap_fma<T>(P, vv[u], acc, w);
-                        else tap_fma1<T>(P, vv[u], acc, w);
+                for (int bx = 0; bx < T::WW; bx += T::GBW) {
+                    unsigned bm[T::MW];
+                    bool hit = false;
+#pragma unroll
+                    for (int q = 0; q < T::MW; q++) {
+                        unsigned gm = 0;
+#pragma unroll
+                        for (int dy = 0; dy < T::GBH; dy++)
+#pragma unroll
+                            for (int dx = 0; dx < T::GBW; dx++) {
+                                const int P = (by + dy) * T::WW + bx + dx;
+                                if (by + dy < T::WH && bx + dx < T::WW && (P >> 5) == q) gm |= 1u << (P & 31);
+                            }
+                        bm[q] = mw[q] & gm;
+                        hit |= bm[q] != 0;
                     }
+                    if (!hit) continue;
+#pragma unroll
+                    for (int dy = 0; dy < T::GBH; dy++)
+#pragma unroll
+                        for (int dx = 0; dx < T::GBW; dx++) {
+                            const int P = (by + dy) * T::WW + bx + dx;
+                            if (by + dy < T::WH && bx + dx < T::WW && ((bm[P >> 5] >> (P & 31)) & 1u)) {
+                                const float v = win[P];
+                                if constexpr (T::PACKED) tap_fma<T>(P, v, acc, w);
+                                else tap_fma1<T>(P, v, acc, w);
+                            }
+                        }
                 }
-            }
         }
         __syncthreads();
     }

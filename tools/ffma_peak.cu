@@ -23,6 +23,24 @@ __global__ void __launch_bounds__(256) ffma_kernel(float* out, float a, float b,
     if (s == 12345.678f) out[0] = s;
 }
 
+template <int ILP>
+__global__ void __launch_bounds__(256) ffma2_kernel(float2* out, float a, float b, int iters) {
+    float2 acc[ILP], w[ILP];
+    const float2 aa = make_float2(a, a);
+#pragma unroll
+    for (int i = 0; i < ILP; i++) { acc[i] = make_float2(threadIdx.x * 1e-3f + i, i); w[i] = make_float2(b + i * 1e-4f, b); }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < ILP; i++) acc[i] = __ffma2_rn(aa, w[i], acc[i]);
+#pragma unroll
+        for (int i = 0; i < ILP; i++) acc[i] = __ffma2_rn(w[i], aa, acc[i]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < ILP; i++) s += acc[i].x + acc[i].y;
+    if (s == 12345.678f) out[0] = make_float2(s, s);
+}
+
 int main() {
     float* out;
     cudaMalloc(&out, 4);
@@ -47,9 +65,21 @@ int main() {
         double tf = flops / (ms * 1e-3) / 1e12;
         if (tf > best) best = tf;
     }
+    float best2 = 0.f;
+    for (int rep = 0; rep < 10; rep++) {
+        cudaEventRecord(e0);
+        ffma2_kernel<16><<<grid, block>>>((float2*)out, 1.0001f, 0.9999f, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 2 * 2 * 16 * (double)iters * grid.x * block.x;
+        double tf = flops / (ms * 1e-3) / 1e12;
+        if (rep > 0 && tf > best2) best2 = tf;
+    }
     int clk = 0;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    printf("{\"ffma_tflops_best\": %.2f, \"sms\": %d, \"max_clock_mhz\": %d, \"nominal_tflops\": %.2f}\n", best, sms,
+    printf("{\"ffma_tflops_best\": %.2f, \"ffma2_tflops_best\": %.2f, \"sms\": %d, \"max_clock_mhz\": %d, \"nominal_tflops\": %.2f}\n", best, best2, sms,
            clk / 1000, sms * 128 * 2 * (clk / 1000.0) * 1e6 / 1e12);
     return 0;
 }
