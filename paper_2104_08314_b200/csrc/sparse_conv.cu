@@ -398,8 +398,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
     const bool w16 = (g.K % 4) == 0;
 
-    for (int c0 = c_begin; c0 < c_end; c0 += T::CH) {
-        const int chn = min(T::CH, c_end - c0);
+    const int CHS = min(T::CH, nwarps);       // channels per chunk: one per warp in P1
+    for (int c0 = c_begin; c0 < c_end; c0 += CHS) {
+        const int chn = min(CHS, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
         // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight); zero the windows
         {
@@ -506,41 +507,25 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                         if constexpr (T::PACKED) w[p][l][m] = make_float2(ws[(2 * p) * 32], ws[(2 * p + 1) * 32]);
                         else w[p][l][m] = ws[p * 32];
                     }
-            // blocks of GBH x GBW window positions: one warp-uniform skip branch per
-            // block (a body of ~8 positions x taps keeps ptxas from if-converting it),
-            // per-position predication inside the block
+            // hierarchical walk: a warp-uniform branch skips each empty group of 4
+            // consecutive window positions, then one per set position
+            const float4* w4 = reinterpret_cast<const float4*>(win);
 #pragma unroll
-            for (int by = 0; by < T::WH; by += T::GBH)
+            for (int q = 0; q < (T::NCASE + 3) / 4; q++) {
+                const unsigned nib = (mw[q >> 3] >> ((q & 7) * 4)) & 0xFu;
+                const float4 v4 = w4[q];
+                if (nib) {
+                    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                for (int bx = 0; bx < T::WW; bx += T::GBW) {
-                    unsigned bm[T::MW];
-                    bool hit = false;
-#pragma unroll
-                    for (int q = 0; q < T::MW; q++) {
-                        unsigned gm = 0;
-#pragma unroll
-                        for (int dy = 0; dy < T::GBH; dy++)
-#pragma unroll
-                            for (int dx = 0; dx < T::GBW; dx++) {
-                                const int P = (by + dy) * T::WW + bx + dx;
-                                if (by + dy < T::WH && bx + dx < T::WW && (P >> 5) == q) gm |= 1u << (P & 31);
-                            }
-                        bm[q] = mw[q] & gm;
-                        hit |= bm[q] != 0;
-                    }
-                    if (!hit) continue;
-#pragma unroll
-                    for (int dy = 0; dy < T::GBH; dy++)
-#pragma unroll
-                        for (int dx = 0; dx < T::GBW; dx++) {
-                            const int P = (by + dy) * T::WW + bx + dx;
-                            if (by + dy < T::WH && bx + dx < T::WW && ((bm[P >> 5] >> (P & 31)) & 1u)) {
-                                const float v = win[P];
-                                if constexpr (T::PACKED) tap_fma<T>(P, v, acc, w);
-                                else tap_fma1<T>(P, v, acc, w);
-                            }
+                    for (int u = 0; u < 4; u++) {
+                        const int P = 4 * q + u;
+                        if (P < T::NCASE && ((nib >> u) & 1u)) {
+                            if constexpr (T::PACKED) tap_fma<T>(P, vv[u], acc, w);
+                            else tap_fma1<T>(P, vv[u], acc, w);
                         }
+                    }
                 }
+            }
         }
         __syncthreads();
     }
