@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspconv.so")
+LIB_PATH = os.environ.get("SPC_LIB_OVERRIDE") or os.path.join(_HERE, "libspconv.so")  # override: dev probes only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2104_08314_b200.build` "

@@ -1,14 +1,17 @@
-"""Build libspconv.so (sm_100a) in-tree with nvcc.  No --use_fast_math: the
-encoder's NZE test must be IEEE (reading A21)."""
+"""Build libspconv.so (sm_100a) in-tree with nvcc: one object per .cu, compiled
+in parallel, then linked.  No --use_fast_math: the encoder's NZE test must be
+IEEE (reading A21)."""
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspconv.so")
+OBJ = os.path.join(HERE, "build")
 SOURCES = ["api.cu", "encode.cu", "sparse_conv.cu", "im2col.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -30,20 +33,27 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, probes: bool = False) -> str:
+    lib = LIB.replace(".so", "_probe.so") if probes else LIB
+    if not force and not probes and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           f"-DSPC_GIT_REV=\"{_git_rev()}\"", "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    obj_dir = OBJ + ("_probe" if probes else "")
+    os.makedirs(obj_dir, exist_ok=True)
+    common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              f"-DSPC_GIT_REV=\"{_git_rev()}\""] + (["-Xptxas=-v"] if verbose else []) + (["-DSPC_PROBES"] if probes else [])
+
+    def compile_one(src: str) -> str:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        subprocess.check_call([*common, "-c", "-o", obj, os.path.join(CSRC, src)])
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"])
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv))

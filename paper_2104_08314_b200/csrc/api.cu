@@ -97,6 +97,7 @@ extern "C" {
 
 const char* spc_last_error(void) { return g_err.c_str(); }
 
+
 const char* spc_version(void) {
 #ifndef SPC_GIT_REV
 #define SPC_GIT_REV "unknown"

@@ -35,25 +35,26 @@ inline Geom make_geom(const spc_conv_desc& d) {
     return g;
 }
 
-// Encoder: 8 warps per CTA; G = 1..8 planes per CTA (8/G warps per plane).
+// Encoder: 8 warps per CTA; a tile = P consecutive channel planes staged in smem.
 constexpr int kEncWarps = 8;
 constexpr int kEncMaxPlaneBytes = 192 * 1024;  // smem stage of one plane
 
-// Decoupled look-back state of the single-pass encoder (lives in the workspace).
+// Cross-CTA prefix state of the single-pass encoder (lives in the workspace).
+// Flags are tagged with epoch+1, so a launch never has to reset them; the CTA
+// that owns the last tile bumps the epoch once every tile has published.
 struct EncState {
-    int ticket;   // dynamic tile counter (CTA start order)
-    int done;     // finished CTAs (the last one resets the state)
-    int pad[2];
+    unsigned epoch;
+    int pad[3];
 };
 
 __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// upper bound on encoder tiles (one plane per CTA), for workspace sizing
+// upper bound on encoder tiles (one plane per tile), for workspace sizing
 inline long long enc_tiles(const Geom& g) { return g.NC; }
 
-// Workspace layout: [EncState | flags[ntiles] | agg[3*ntiles] | inc[3*ntiles] | cps_in[da_cap]]
+// Workspace layout: [EncState | flags[ntiles] (u64) | agg[3*ntiles] | cps_in[da_cap]]
 struct WsLayout {
-    size_t state, flags, agg, inc, cps_in, total;
+    size_t state, flags, agg, cps_in, total;
 };
 
 inline WsLayout ws_layout(const Geom& g) {
@@ -61,12 +62,48 @@ inline WsLayout ws_layout(const Geom& g) {
     long long nt = enc_tiles(g);
     L.state = 0;
     L.flags = align_up(sizeof(EncState), 256);
-    L.agg = align_up(L.flags + sizeof(int) * (size_t)nt, 256);
-    L.inc = align_up(L.agg + sizeof(long long) * 3 * (size_t)nt, 256);
-    L.cps_in = align_up(L.inc + sizeof(long long) * 3 * (size_t)nt, 256);
+    L.agg = align_up(L.flags + sizeof(unsigned long long) * (size_t)nt, 256);
+    L.cps_in = align_up(L.agg + sizeof(long long) * 3 * (size_t)nt, 256);
     L.total = align_up(L.cps_in + sizeof(int32_t) * (size_t)(g.NC * g.H * g.W), 256);
     return L;
 }
+
+// Development probes (built only with -DSPC_PROBES): thread 0 of every CTA
+// stamps %globaltimer and clock64 at phase boundaries into a per-TU buffer;
+// spc_debug_probes_<tu>() copies it out.  Compiled out of the product library.
+constexpr int kProbeCtas = 1024, kProbeSlots = 16;
+#ifdef SPC_PROBES
+static __device__ unsigned long long g_probe[kProbeCtas][kProbeSlots][2];
+#define SPC_PROBE_ACCESSOR(name)                                                                 \
+    extern "C" int name(unsigned long long* host, int clear) {                                   \
+        cudaDeviceSynchronize();                                                                 \
+        if (cudaMemcpyFromSymbol(host, spc::g_probe, sizeof(spc::g_probe)) != cudaSuccess) return -1; \
+        if (clear) {                                                                             \
+            void* p = nullptr;                                                                   \
+            cudaGetSymbolAddress(&p, spc::g_probe);                                              \
+            cudaMemset(p, 0, sizeof(spc::g_probe));                                              \
+        }                                                                                        \
+        return 0;                                                                                \
+    }
+__device__ __forceinline__ void probe(int slot) {
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x + blockIdx.z * gridDim.x * gridDim.y < kProbeCtas) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const unsigned b = blockIdx.x + blockIdx.y * gridDim.x + blockIdx.z * gridDim.x * gridDim.y;
+        g_probe[b][slot][0] = t;
+        g_probe[b][slot][1] = clock64();
+    }
+}
+#else
+__device__ __forceinline__ void probe(int) {}
+#endif
+
+// Programmatic dependent launch (sm_90+): a secondary kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization starts while its primary
+// still runs; pdl_wait() blocks until the primary grid has completed and its
+// memory is visible (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---- device helpers --------------------------------------------------------
 
@@ -84,6 +121,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <typename T>

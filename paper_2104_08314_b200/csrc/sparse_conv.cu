@@ -136,6 +136,88 @@ __device__ __forceinline__ void column_range(const Geom& g, const int32_t* __res
     column_range_rel(g, seg, d, w, lo, hi);
 }
 
+// Compile-time-S variant for the strip kernel: fully unrolled, so the
+// directory stays in registers (a runtime-indexed ChanDir spills to local memory).
+template <int S>
+struct DirS {
+    int npc;
+    int pos[S];
+    int da[S];
+};
+
+template <int S>
+__device__ __forceinline__ void parse_dir(const Geom& g, const int32_t* seg, DirS<S>& d) {
+#pragma unroll
+    for (int t = 0; t < S; t++) { d.pos[t] = -1; d.da[t] = 0; }
+    d.npc = (seg[0] == SPC_NPC);
+    if (d.npc) return;
+    if (S == 1) {                                // SI Alg. 5: [0, c_0 .. c_{Ow-1}]
+        d.pos[0] = 1;
+        return;
+    }
+    int p = 0, dacur = 0;
+    if (g.pl == 0) {                             // NOP [0, a, a+b]
+        d.pos[0] = 1;
+        dacur = seg[2];
+        p = 3;
+    }
+#pragma unroll
+    for (int t = 1; t < S; t++) {
+        if (t < g.pl) continue;                  // pad columns own no block
+        if (seg[p + 1] == SPC_NPF) {            // skip pointer
+            p += 2;
+            continue;
+        }
+        d.pos[t] = p + 1;
+        d.da[t] = dacur;
+        const int last = (t < S - 1) ? (g.Ow1 - 1 - t) : (g.Ow1 - S);
+        dacur += seg[p + 1 + last];
+        p += 1 + g.Ow1;
+    }
+}
+
+template <int S>
+__device__ __forceinline__ int sel(const int (&arr)[S], int t) {
+    int v = arr[0];
+#pragma unroll
+    for (int i = 1; i < S; i++)
+        if (t == i) v = arr[i];
+    return v;
+}
+
+// DA range [lo, hi) (channel-relative) of padded column w (compile-time S).
+template <int S>
+__device__ __forceinline__ void column_range_s(const Geom& g, const int32_t* seg, const DirS<S>& d, int w,
+                                               int& lo, int& hi) {
+    lo = hi = 0;
+    if (w < 0 || w >= g.Wp) return;
+    if (S == 1) {
+        lo = (w == 0) ? 0 : seg[d.pos[0] + w - 1];
+        hi = seg[d.pos[0] + w];
+        return;
+    }
+    if (w >= S - 1 && w <= g.Wp - S) {                        // overlapK_w column of partition s
+        const int s = w - S + 1;
+        if (d.pos[S - 1] < 0) return;
+        lo = d.da[S - 1] + ((s == 0) ? 0 : seg[d.pos[S - 1] + s - 1]);
+        hi = d.da[S - 1] + seg[d.pos[S - 1] + s];
+        return;
+    }
+    const bool left = w < S - 1;
+    const int t = left ? w : (g.Wp - 1 - w);
+    const int pos = sel(d.pos, t), dat = sel(d.da, t);
+    if (t < g.pl || pos < 0) return;                          // pad column or NPF block
+    if (t == 0) {                                             // NOP: col 0 then col Wp-1
+        const int a = seg[pos];
+        if (left) { lo = 0; hi = a; }
+        else { lo = a; hi = seg[pos + 1]; }
+        return;
+    }
+    const int c0 = seg[pos];                                  // left column owned by partition 0
+    if (left) { lo = dat; hi = dat + c0; }
+    else { lo = dat + c0; hi = dat + seg[pos + g.Ow1 - 1 - t]; }
+}
+
 // -------------------------------------------------------- CPS expansion
 
 // Alg. 4 index reconstruction for the overlapK_w block:
@@ -154,6 +236,8 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
                                                          int32_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const long long nc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    pdl_wait();
+    pdl_trigger();
     if (nc >= g.NC) return;
     const long long Z = cnz_off[nc], Q = cin_off[nc];
     const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q);
@@ -206,9 +290,18 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st) {
     const int wpb = 8;
     long long blocks = (g.NC + wpb - 1) / wpb;
-    cps_expand_kernel<<<(unsigned)blocks, wpb * 32, 0, st>>>(g, e->ptr, e->in, e->chan_ptr_off, e->chan_nz_off,
-                                                            e->chan_in_off, in_cpo);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(wpb * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, cps_expand_kernel, g, (const int32_t*)e->ptr, (const int32_t*)e->in,
+                              (const int64_t*)e->chan_ptr_off, (const int64_t*)e->chan_nz_off,
+                              (const int64_t*)e->chan_in_off, in_cpo);
 }
 
 // ------------------------------------------------------------ conv kernels
@@ -399,6 +492,30 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     const bool w16 = (g.K % 4) == 0;
 
     const int CHS = min(T::CH, nwarps);       // channels per chunk: one per warp in P1
+    // taps W[c][l][m][kbase..+KB) of a chunk -> s_w (cp.async); independent of the encoding
+    auto stage_w = [&](int c0, int chn) {
+        const float* wsrc = a.wp + (long long)c0 * T::RS * g.K + kbase;   // row (j*RS+rs) at stride K
+        const int rows = chn * T::RS;
+        if (w16) {
+            constexpr int VPR = T::KB / 4;                 // 16-byte vectors per row
+            const int vq = threadIdx.x % VPR, kq = 4 * vq;
+            const int nb = max(0, min(16, 4 * (g.K - (kbase + kq))));
+            for (int r = threadIdx.x / VPR; r < rows; r += nthreads / VPR)
+                cp_async16(s_w + r * T::KB + kq, wsrc + (long long)r * g.K + (nb ? kq : 0), nb);
+        } else {
+            for (int i = threadIdx.x; i < rows * T::KB; i += nthreads) {
+                const int kk = i % T::KB, r = i / T::KB;
+                const bool ok = kbase + kk < g.K;
+                cp_async4(s_w + i, wsrc + (long long)r * g.K + (ok ? kk : 0), ok ? 4 : 0);
+            }
+        }
+    };
+    // PDL prologue: the first chunk's taps load while the encoder finishes
+    probe(0);
+    if (c_begin < c_end) stage_w(c_begin, min(CHS, c_end - c_begin));
+    probe(1);
+    pdl_wait();
+    probe(2);
     for (int c0 = c_begin; c0 < c_end; c0 += CHS) {
         const int chn = min(CHS, c_end - c0);
         const long long nc0 = (long long)n * g.C + c0;
@@ -412,34 +529,21 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
                 s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
             }
-            const float* wsrc = a.wp + (long long)c0 * T::RS * g.K + kbase;   // row (j*RS+rs) at stride K
-            const int rows = chn * T::RS;
-            if (w16) {
-                constexpr int VPR = T::KB / 4;                 // 16-byte vectors per row
-                const int vq = threadIdx.x % VPR, kq = 4 * vq;
-                const int nb = max(0, min(16, 4 * (g.K - (kbase + kq))));
-                for (int r = threadIdx.x / VPR; r < rows; r += nthreads / VPR)
-                    cp_async16(s_w + r * T::KB + kq, wsrc + (long long)r * g.K + (nb ? kq : 0), nb);
-            } else {
-                for (int i = threadIdx.x; i < rows * T::KB; i += nthreads) {
-                    const int kk = i % T::KB, r = i / T::KB;
-                    const bool ok = kbase + kk < g.K;
-                    cp_async4(s_w + i, wsrc + (long long)r * g.K + (ok ? kk : 0), ok ? 4 : 0);
-                }
-            }
+            if (c0 != c_begin) stage_w(c0, chn);
             float4* v4 = reinterpret_cast<float4*>(s_val);
             for (int i = threadIdx.x; i < chn * RT * T::NCP / 4; i += nthreads) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             cp_async_wait_all();
         }
         __syncthreads();
+        if (c0 == c_begin) probe(3);
         // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
         for (int j = warp; j < chn; j += nwarps) {
             const int* seg = s_ptr + s_poff[j];
-            ChanDir d;
-            parse_channel_rel(g, seg, d);
+            DirS<T::S> d;
+            parse_dir<T::S>(g, seg, d);
             if (d.npc) continue;                                  // NPC: skip channel
             int lo = 0, hi = 0;
-            if (lane < T::WW) column_range_rel(g, seg, d, wx0 + lane, lo, hi);
+            if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
             int tot;
             const int pre = warp_exclusive_scan(hi - lo, &tot);
             int* spre = s_scr + warp * 64;
@@ -484,6 +588,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
         __syncthreads();
+        if (c0 == c_begin) probe(4);
         // ---- P2: unrolled walk over the window positions of this warp's row tile
         for (int j = cs; j < chn; j += CS) {
             const float* win = s_val + (j * RT + rtile) * T::NCP;
@@ -530,6 +635,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         __syncthreads();
     }
 
+    probe(5);
     // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
     constexpr int TT = T::TY * T::TX, TP = TT + 1;
     float accf[T::NACC];   // index kk*TT + t
@@ -564,7 +670,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 #pragma unroll
         for (int i = 0; i < T::NACC; i++) part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = accf[i];
     }
+    probe(6);
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
+    probe(7);
     // ---- sum the cluster's partials (DSMEM), ReLU, store NKHW (t = ty*TX + tx fastest)
     static_assert((TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "power-of-two tile and k block");
     const int total = RT * T::KB * TT;
@@ -579,19 +687,18 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
         }
     } else {
-        float* peers[8];
-#pragma unroll
-        for (int r = 0; r < 8; r++) peers[r] = (r < a.cg) ? cgrp::this_cluster().map_shared_rank(part, r) : nullptr;
+        auto cl = cgrp::this_cluster();
         for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
             const int t = i & (TT - 1), rk = i / TT, kl = rk & (T::KB - 1), rr = rk / T::KB;
             const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + (t & (T::TX - 1));
             const int sidx = rk * TP + t;
             float sum = 0.f;
-            for (int r = 0; r < a.cg; r++) sum += peers[r][sidx];
+            for (int r = 0; r < a.cg; r++) sum += cl.map_shared_rank(part, r)[sidx];
             if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
         }
         cgrp::this_cluster().sync();
     }
+    probe(8);
 }
 
 // Generic variant: any R, S, stride; TY x TX = 4 x 4 tile, accumulators in smem.
@@ -612,6 +719,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
     float* acc = accs + warp * kGenTY * kGenTX * 32;
     for (int i = 0; i < kGenTY * kGenTX; i++) acc[i * 32 + lane] = 0.f;
     const int k = kbase + lane;
+    pdl_wait();
     for (int c = warp; c < g.C; c += kGenWarps) {
         const long long nc = (long long)n * g.C + c;
         ChanDir d;
@@ -702,13 +810,15 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(32 * a.rt * a.csplit);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = cg;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T>, a);
 }
 
@@ -753,8 +863,21 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     err = cudaFuncSetAttribute(sparse_conv_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     dim3 grid(a.tiles_x * ty, (g.K + 31) / 32, g.N);
-    sparse_conv_generic_kernel<<<grid, kGenWarps * 32, smem, st>>>(a, WH, WW);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kGenWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, sparse_conv_generic_kernel, a, WH, WW);
 }
 
 }  // namespace spc
+
+#ifdef SPC_PROBES
+SPC_PROBE_ACCESSOR(spc_debug_probes_conv)
+#endif
