@@ -36,15 +36,16 @@ inline Geom make_geom(const spc_conv_desc& d) {
 }
 
 // Encoder: 8 warps per CTA; a tile = P consecutive channel planes staged in smem.
-constexpr int kEncWarps = 8;
+constexpr int kEncWarps = 16;
 constexpr int kEncMaxPlaneBytes = 192 * 1024;  // smem stage of one plane
 
 // Cross-CTA prefix state of the single-pass encoder (lives in the workspace).
-// Flags are tagged with epoch+1, so a launch never has to reset them; the CTA
-// that owns the last tile bumps the epoch once every tile has published.
+// Aggregates are tagged with epoch+1, so a launch never has to reset them; the
+// CTA that owns the last tile bumps the epoch once every tile has published.
 struct EncState {
     unsigned epoch;
-    int pad[3];
+    unsigned count[2];   // tiles published in launch e (slot e & 1); the other slot is reset for e+1
+    int pad;
 };
 
 __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -106,6 +107,27 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---- device helpers --------------------------------------------------------
+
+// 1D TMA bulk copies (cp.async.bulk) into shared memory, completion counted on an
+// mbarrier in transaction bytes.  Sizes and addresses are multiples of 16 bytes.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;

@@ -30,8 +30,10 @@ namespace spc {
 namespace {
 
 constexpr int kThreads = kEncWarps * 32;
+constexpr unsigned kBulkChunk = 1u << 15;   // bytes per cp.async.bulk
 constexpr int kTagShift = 40;
 constexpr unsigned long long kValMask = (1ull << kTagShift) - 1;
+constexpr int kTabIn = 1 << 16, kTabOk = 1 << 17;   // column-table flags (low 16 bits: local column)
 
 struct EncArgs {
     Geom g;
@@ -53,6 +55,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
 }
 __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // padded column at position `pos` of the canonical stream order:
@@ -79,21 +89,45 @@ __device__ __forceinline__ bool is_middle(const Geom& g, int w) {
 
 // shared-memory carve-up of one tile (host and device agree through this)
 struct EncSmem {
-    size_t planes, msk, cnt, incnt, dab, inb, pinfo, poff, total;
+    size_t planes, umask, msk, cnt, incnt, dab, inb, tab, pinfo, poff, total;
 };
 __host__ __device__ inline EncSmem enc_smem_layout(const Geom& g, int P) {
     EncSmem L;
     const size_t HW = (size_t)g.H * g.W, cols = (size_t)P * g.Wp;
+    const size_t nrb = (g.H + 31) / 32;
     L.planes = 0;
-    L.msk = align_up((P * HW + 8) * sizeof(float), 16);
+    L.umask = align_up((P * HW + 8) * sizeof(float), 16);          // [P][W][nrb] unpadded column masks
+    L.msk = align_up(L.umask + (size_t)P * g.W * nrb * sizeof(unsigned), 16);
     L.cnt = align_up(L.msk + cols * g.nwords * sizeof(unsigned), 16);
     L.incnt = L.cnt + cols * sizeof(int);
     L.dab = L.incnt + cols * sizeof(int);
     L.inb = L.dab + cols * sizeof(int);
-    L.pinfo = align_up(L.inb + cols * sizeof(int), 16);            // [P][4]: plen, nnz, in_len, lower
+    L.tab = align_up(L.inb + cols * sizeof(int), 16);              // [P][Wp] int4 column table
+    L.pinfo = align_up(L.tab + cols * sizeof(int4), 16);           // [P][4]: plen, nnz, in_len, lower
     L.poff = align_up(L.pinfo + (size_t)P * 4 * sizeof(int), 16);   // [P][4] int64: ptr, da, in offsets, fits
     L.total = align_up(L.poff + (size_t)P * 4 * sizeof(long long), 16);
     return L;
+}
+
+// ptr length (NPC | S=1 block | NOP + overlap blocks with NPF, SI Eq. 3), and the DA
+// count below the overlapK_w block, of one plane with column counts wc and totals td, ti
+__device__ __forceinline__ void plane_lengths(const Geom& g, const int* wc, int td, int ti, int* pi) {
+    int plen, lower = 0;
+    if (td == 0) {
+        plen = 1;                                   // NPC
+    } else if (g.S == 1) {
+        plen = 1 + g.Ow1;
+    } else {
+        plen = (g.pl == 0) ? 3 : 0;                 // NOP block (reading A2)
+        for (int t = max(1, g.pl); t <= g.S - 2; t++) {
+            const int bn = wc[t] + wc[g.Wp - 1 - t];
+            lower += bn;
+            plen += bn ? (1 + g.Ow1) : 2;           // block or [tag, NPF] (reading A3)
+        }
+        if (g.pl == 0) lower += wc[0] + wc[g.Wp - 1];
+        plen += (td - lower) ? (1 + g.Ow1) : 2;
+    }
+    pi[0] = plen; pi[1] = td; pi[2] = ti; pi[3] = lower;
 }
 
 template <bool CPS>
@@ -104,6 +138,8 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
     __shared__ long long s_tile_tot[3];
     __shared__ long long s_pre[3];
     __shared__ unsigned s_epoch;
+    __shared__ __align__(8) unsigned long long s_bar[1];
+    unsigned s_phase = 0;   // (per thread) parity of the staging barrier
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int HW = g.H * g.W, Wp = g.Wp, NW = g.nwords;
 
@@ -111,7 +147,12 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
     pdl_wait();      // x may come from the kernel before us
     probe(1);
     pdl_trigger();   // the dependent convolution may launch and stage its taps
-    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(&a.st->epoch);
+    if (threadIdx.x == 0) {
+        s_epoch = *reinterpret_cast<volatile unsigned*>(&a.st->epoch);
+        mbar_init(s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
 
     const EncSmem L = enc_smem_layout(g, a.P);
     float* planes = reinterpret_cast<float*>(smem_raw + L.planes);
@@ -120,6 +161,9 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
     int* incnt = reinterpret_cast<int*>(smem_raw + L.incnt);
     int* dab = reinterpret_cast<int*>(smem_raw + L.dab);
     int* inb = reinterpret_cast<int*>(smem_raw + L.inb);
+    unsigned* umask = reinterpret_cast<unsigned*>(smem_raw + L.umask);
+    int4* tab = reinterpret_cast<int4*>(smem_raw + L.tab);
+    const int NRB = (g.H + 31) / 32;
     int* pinfo = reinterpret_cast<int*>(smem_raw + L.pinfo);
     long long* poff = reinterpret_cast<long long*>(smem_raw + L.poff);
 
@@ -127,55 +171,86 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
         const long long plane0 = (long long)tile * a.P;
         const int np = (int)min((long long)a.P, g.NC - plane0);
 
-        // ---- 1. stage the tile's planes: 128-bit loads from the 16-byte aligned
-        //         element a0 <= e0 (x is 16-byte aligned), four in flight per thread
+        // ---- 1. stage the tile's planes with TMA bulk copies (one elected thread, the whole
+        //         tile in flight) from the 16-byte aligned element a0 <= e0; the < 16-byte tail
+        //         with plain loads (x is 16-byte aligned)
         const long long e0 = plane0 * HW, e1 = e0 + (long long)np * HW;
         const long long a0 = e0 & ~3ll;
         const int sh = (int)(e0 - a0);
         {
-            const long long n4 = (e1 - a0) >> 2;
-            const float4* s4 = reinterpret_cast<const float4*>(a.x + a0);
-            float4* d4 = reinterpret_cast<float4*>(planes);
-            for (long long i = threadIdx.x; i < n4; i += 4 * kThreads) {
-                float4 v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (i + u * kThreads < n4) v[u] = __ldg(s4 + i + u * kThreads);
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (i + u * kThreads < n4) d4[i + u * kThreads] = v[u];
+            const long long n4 = (e1 - a0) >> 2;        // whole 16-byte vectors
+            if (threadIdx.x == 0) {
+                const unsigned bytes = (unsigned)(n4 * 16);
+                mbar_expect_tx(s_bar, bytes);
+                const char* src = reinterpret_cast<const char*>(a.x + a0);
+                char* dst = reinterpret_cast<char*>(planes);
+                for (unsigned off = 0; off < bytes; off += kBulkChunk)
+                    bulk_g2s(dst + off, src + off, min(kBulkChunk, bytes - off), s_bar);
             }
             for (long long i = a0 + 4 * n4 + threadIdx.x; i < e1; i += kThreads) planes[i - a0] = __ldg(a.x + i);
+            mbar_wait(s_bar, s_phase);
+            s_phase ^= 1u;
         }
         __syncthreads();
         probe(2);
         const float* pl0 = planes + sh;
 
-        // ---- 2. column bitmasks in the padded frame: item = (plane, word, column), column fastest
-        for (int it = threadIdx.x; it < np * NW * Wp; it += kThreads) {
-            const int w = it % Wp, pj = it / Wp, j = pj % NW, p = pj / NW;
-            const int wu = w - g.pl;
-            unsigned m = 0;
-            if (wu >= 0 && wu < g.W) {
-                const int h0 = 32 * j - g.pt;
-                const int b0 = max(0, -h0), b1 = min(32, g.H - h0);
-                const float* col = pl0 + (size_t)p * HW + wu;
+        // ---- 2. unpadded column bitmasks by warp ballots + a 32x32 bit transpose:
+        //         block = (plane group, 32-row block, 32-column block); for W <= 32 one
+        //         warp covers G = 32/W planes (lane l -> plane l/W, column l%W)
+        {
+            const int G = (g.W <= 32) ? (32 / g.W) : 1;
+            const int CBW = (g.W <= 32) ? g.W : 32;            // columns per lane group
+            const int NCB = (g.W + 31) / 32;
+            const int npg = (np + G - 1) / G;
+            const int p_l = lane / CBW, c_l = lane % CBW;
+            for (int blk = warp; blk < npg * NRB * NCB; blk += kEncWarps) {
+                const int cb = blk % NCB, rb = (blk / NCB) % NRB, pg = blk / (NCB * NRB);
+                const int p = pg * G + p_l, col = cb * 32 + c_l;
+                const bool ok = (lane < G * CBW) && (p < np) && (col < g.W);
+                const float* src = pl0 + (size_t)(ok ? p : 0) * HW + (ok ? col : 0);
+                unsigned x = 0;
 #pragma unroll
-                for (int b = 0; b < 32; b++)
-                    if (b >= b0 && b < b1) m |= (unsigned)(col[(h0 + b) * g.W] != 0.0f) << b;
+                for (int r0 = 0; r0 < 32; r0 += 8) {
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++)      // unconditional (clamped) loads, all in flight
+                        v[u] = src[min(rb * 32 + r0 + u, g.H - 1) * g.W];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const bool nz = ok && (rb * 32 + r0 + u < g.H) && (v[u] != 0.0f);
+                        const unsigned b = __ballot_sync(0xffffffffu, nz);
+                        x = (lane == r0 + u) ? b : x;
+                    }
+                }
+                // lane r holds row r (bit l = lane-column l); transpose -> lane l holds column l
+#pragma unroll
+                for (int sft = 16; sft >= 1; sft >>= 1) {
+                    const unsigned M = (sft == 16) ? 0x0000FFFFu : (sft == 8) ? 0x00FF00FFu
+                                     : (sft == 4) ? 0x0F0F0F0Fu : (sft == 2) ? 0x33333333u : 0x55555555u;
+                    const unsigned y = __shfl_xor_sync(0xffffffffu, x, sft);
+                    x = (lane & sft) ? ((x & ~M) | ((y & ~M) >> sft)) : ((x & M) | ((y & M) << sft));
+                }
+                if (ok) umask[((size_t)p * g.W + col) * NRB + rb] = x;
             }
-            msk[(p * Wp + w) * NW + j] = m;
         }
         __syncthreads();
-
         probe(3);
-        // ---- 3. per column: NZE count and IN entries (CPS set4 packing in overlapK_w)
+        // ---- 3. padded masks (shift by pad_top), per-column NZE count and IN entries
+        //         (CPS set4 packing in overlapK_w)
         for (int it = threadIdx.x; it < np * Wp; it += kThreads) {
-            const int w = it % Wp;
+            const int w = it % Wp, p = it / Wp;
+            const int col = w - g.pl;
+            const bool real = col >= 0 && col < g.W;
+            const unsigned* u = umask + ((size_t)p * g.W + (real ? col : 0)) * NRB;
             int c = 0, e = 0;
             const bool mid = CPS && is_middle(g, w);
+            unsigned prev = 0;
             for (int j = 0; j < NW; j++) {
-                const unsigned m = msk[it * NW + j];
+                const unsigned uj = (real && j < NRB) ? u[j] : 0u;
+                const unsigned m = g.pt ? ((uj << g.pt) | (prev >> (32 - g.pt))) : uj;
+                prev = uj;
+                msk[it * NW + j] = m;
                 c += __popc(m);
                 if (mid) {
 #pragma unroll
@@ -189,49 +264,47 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             incnt[it] = mid ? e : c;
         }
         __syncthreads();
-
         probe(4);
-        // ---- 4. per plane (warp per plane): stream-order exclusive prefix over columns,
-        //         plane totals and the ptr length (SI Eq. 3 with the actual NPF count)
-        for (int p = warp; p < np; p += kEncWarps) {
-            const int* wc = cnt + p * Wp;
-            const int* wi = incnt + p * Wp;
-            const int per = (Wp + 31) / 32;
-            const int q0 = lane * per, q1 = min(q0 + per, Wp);
-            int sd = 0, si = 0;
-            for (int q = q0; q < q1; q++) {
-                const int w = col_at(g, q);
-                sd += wc[w];
-                si += wi[w];
-            }
-            int td, ti;
-            int ed = warp_exclusive_scan(sd, &td);
-            int ei = warp_exclusive_scan(si, &ti);
-            for (int q = q0; q < q1; q++) {
-                const int w = col_at(g, q);
-                dab[p * Wp + w] = ed;
-                inb[p * Wp + w] = ei;
-                ed += wc[w];
-                ei += wi[w];
-            }
-            if (lane == 0) {
-                int plen, lower = 0;
-                if (td == 0) {
-                    plen = 1;                                   // NPC
-                } else if (g.S == 1) {
-                    plen = 1 + g.Ow1;
-                } else {
-                    plen = (g.pl == 0) ? 3 : 0;                 // NOP block (reading A2)
-                    for (int t = max(1, g.pl); t <= g.S - 2; t++) {
-                        const int bn = wc[t] + wc[Wp - 1 - t];
-                        lower += bn;
-                        plen += bn ? (1 + g.Ow1) : 2;           // block or [tag, NPF] (reading A3)
-                    }
-                    if (g.pl == 0) lower += wc[0] + wc[Wp - 1];
-                    plen += (td - lower) ? (1 + g.Ow1) : 2;
+        // ---- 4. per plane: stream-order exclusive prefix over columns, plane totals and
+        //         the ptr length (SI Eq. 3 with the actual NPF count); thread per plane for
+        //         narrow planes, warp per plane otherwise
+        if (Wp <= 24) {
+            for (int p = threadIdx.x; p < np; p += kThreads) {
+                const int* wc = cnt + p * Wp;
+                const int* wi = incnt + p * Wp;
+                int ed = 0, ei = 0;
+                for (int q = 0; q < Wp; q++) {
+                    const int w = col_at(g, q);
+                    dab[p * Wp + w] = ed;
+                    inb[p * Wp + w] = ei;
+                    ed += wc[w];
+                    ei += wi[w];
                 }
-                int* pi = pinfo + 4 * p;
-                pi[0] = plen; pi[1] = td; pi[2] = ti; pi[3] = lower;
+                plane_lengths(g, wc, ed, ei, pinfo + 4 * p);
+            }
+        } else {
+            for (int p = warp; p < np; p += kEncWarps) {
+                const int* wc = cnt + p * Wp;
+                const int* wi = incnt + p * Wp;
+                const int per = (Wp + 31) / 32;
+                const int q0 = lane * per, q1 = min(q0 + per, Wp);
+                int sd = 0, si = 0;
+                for (int q = q0; q < q1; q++) {
+                    const int w = col_at(g, q);
+                    sd += wc[w];
+                    si += wi[w];
+                }
+                int td, ti;
+                int ed = warp_exclusive_scan(sd, &td);
+                int ei = warp_exclusive_scan(si, &ti);
+                for (int q = q0; q < q1; q++) {
+                    const int w = col_at(g, q);
+                    dab[p * Wp + w] = ed;
+                    inb[p * Wp + w] = ei;
+                    ed += wc[w];
+                    ei += wi[w];
+                }
+                if (lane == 0) plane_lengths(g, wc, td, ti, pinfo + 4 * p);
             }
         }
         __syncthreads();
@@ -256,22 +329,35 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
         __syncthreads();
 
         probe(6);
-        // ---- 6. publish the tile aggregate; prefix = sum over ALL preceding tiles
+        // ---- 6. publish the tile aggregate (tagged words + a per-launch counter),
+        //         wait for every tile of this round, prefix = sum over ALL preceding tiles
         const unsigned long long tag = (unsigned long long)((s_epoch + 1u) & 0xFFFFFFu);
-        if (threadIdx.x < 3)
-            st_relaxed64(a.agg + 3ll * tile + threadIdx.x, (tag << kTagShift) | (unsigned long long)s_tile_tot[threadIdx.x]);
+        unsigned* counter = &a.st->count[s_epoch & 1u];
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < 3; i++)
+                st_relaxed64(a.agg + 3ll * tile + i, (tag << kTagShift) | (unsigned long long)s_tile_tot[i]);
+            red_release_add(counter, 1u);
+            const unsigned target = (unsigned)min(a.ntiles, (tile / (int)gridDim.x + 1) * (int)gridDim.x);
+            long long spin = 0;
+            while (ld_acquire_u32(counter) < target) {
+                __nanosleep(32);
+                if (++spin > (1ll << 24)) __trap();   // bounded: never hang the GPU
+            }
+        }
+        __syncthreads();
         {
             long long p0 = 0, p1 = 0, p2 = 0;
             for (long long i = threadIdx.x; i < 3ll * tile; i += kThreads) {
                 unsigned long long v;
                 long long spin = 0;
                 while (((v = ld_relaxed64(a.agg + i)) >> kTagShift) != tag)
-                    if (++spin > (1ll << 26)) __trap();   // bounded: never hang the GPU
+                    if (++spin > (1ll << 24)) __trap();
                 const long long val = (long long)(v & kValMask);
-                const int s = (int)(i % 3);
-                p0 += (s == 0) ? val : 0;
-                p1 += (s == 1) ? val : 0;
-                p2 += (s == 2) ? val : 0;
+                const int sidx = (int)(i % 3);
+                p0 += (sidx == 0) ? val : 0;
+                p1 += (sidx == 1) ? val : 0;
+                p2 += (sidx == 2) ? val : 0;
             }
             p0 = warp_sum(p0); p1 = warp_sum(p1); p2 = warp_sum(p2);
             if (lane == 0) { s_red[warp][0] = p0; s_red[warp][1] = p1; s_red[warp][2] = p2; }
@@ -295,6 +381,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             a.lengths[1] = t1;
             a.lengths[2] = t2;
             a.lengths[3] = (t0 > a.cap_ptr || t1 > a.cap_da || t2 > a.cap_in) ? 1 : 0;
+            a.st->count[(s_epoch + 1u) & 1u] = 0;   // the next launch's counter (unused in this one)
             a.st->epoch = s_epoch + 1u;
         }
         for (int p = threadIdx.x; p < np; p += kThreads) {
@@ -305,6 +392,17 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             poff[4 * p] = P; poff[4 * p + 1] = Z; poff[4 * p + 2] = Q;
             poff[4 * p + 3] = (P + pinfo[4 * p] <= a.cap_ptr) && (Z + pinfo[4 * p + 1] <= a.cap_da) &&
                               (Q + pinfo[4 * p + 2] <= a.cap_in);
+        }
+        __syncthreads();
+        // per-column table for the DA/IN pass: tile-relative DA / IN offsets of the column,
+        // smem index of its padded row 0, local column L and flags (no divisions later)
+        for (int it = threadIdx.x; it < np * Wp; it += kThreads) {
+            const int p = it / Wp, w = it % Wp;
+            const bool ok = poff[4 * p + 3] && cnt[it] > 0;
+            const bool wr_in = !(CPS && is_middle(g, w));
+            tab[it] = make_int4((int)(poff[4 * p + 1] - Z0) + dab[it], (int)(poff[4 * p + 2] - Q0) + inb[it],
+                                p * HW + (w - g.pl) - g.pt * g.W,
+                                local_of(g, w) | (wr_in ? kTabIn : 0) | (ok ? kTabOk : 0));
         }
         __syncthreads();
 
@@ -357,57 +455,116 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
         }
 
         probe(9);
-        // ---- 7b. DA / IN, column by column (G of Alg. 1), warp per (plane, column)
-        for (int it = warp; it < np * Wp; it += kEncWarps) {
-            if (cnt[it] == 0) continue;
-            const int p = it / Wp, w = it % Wp;
-            if (!poff[4 * p + 3]) continue;
-            const int L = local_of(g, w);
-            const int wu = w - g.pl;
-            const float* pl = pl0 + (size_t)p * HW;
-            float* dd = a.da + poff[4 * p + 1] + dab[it];
-            int32_t* ii = a.in + poff[4 * p + 2] + inb[it];
-            const bool mid = CPS && is_middle(g, w);
-            int run = 0, irun = 0;
-            for (int j = 0; j < NW; j++) {
-                const unsigned m = msk[it * NW + j];
-                if (m == 0) continue;
-                const int h = 32 * j + lane;
-                if ((m >> lane) & 1u) {
-                    const int r = run + __popc(m & lanemask_lt());
-                    dd[r] = pl[(h - g.pt) * g.W + wu];
-                    if (!mid) ii[r] = L + h * g.S;
-                }
-                run += __popc(m);
-                if (mid) {
-                    // set4 packing: lanes 0..7 own the 8 nibbles of this word
-                    int k = 0, e = 0;
-                    unsigned nib = 0;
-                    if (lane < 8) {
-                        nib = (m >> (4 * lane)) & 0xFu;
-                        k = __popc(nib);
-                        e = k >= 3 ? 2 : k;
+        // ---- 7b. DA (and CPO-form IN): lanes = rows of a column word; the rank of an NZE
+        //          is a popc of the mask below its lane (coalesced stores).  Short columns
+        //          (one word, Hp <= 16) pack 32/Hp columns into a warp pass.
+        {
+            float* dT = a.da + Z0;
+            int32_t* iT = a.in + Q0;
+            const int nit = np * Wp;
+            if (NW == 1 && g.Hp <= 16) {
+                const int CPW = 32 / g.Hp;
+                const int sub = lane / g.Hp, row = lane - sub * g.Hp;
+                for (int it0 = warp * CPW; it0 < nit; it0 += kEncWarps * CPW) {
+                    const int it = it0 + sub;
+                    const unsigned m = (sub < CPW && it < nit) ? msk[it] : 0u;
+                    if ((m >> row) & 1u) {
+                        const int4 t = tab[it];
+                        if (t.w & kTabOk) {
+                            const int r = __popc(m & ((1u << row) - 1u));
+                            dT[t.x + r] = pl0[t.z + row * g.W];
+                            if (t.w & kTabIn) iT[t.y + r] = (t.w & 0xFFFF) + row * g.S;
+                        }
                     }
+                }
+            } else if (NW <= 2) {
+                // two column items per warp iteration: table and mask loads of both in flight
+                for (int it0 = 2 * warp; it0 < nit; it0 += 2 * kEncWarps) {
+                    int4 t[2];
+                    unsigned m[2][2];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const bool v = it0 + u < nit;
+                        t[u] = v ? tab[it0 + u] : make_int4(0, 0, 0, 0);
+                        m[u][0] = v ? msk[(it0 + u) * NW] : 0u;
+                        m[u][1] = (v && NW == 2) ? msk[(it0 + u) * NW + 1] : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        if (!(t[u].w & kTabOk)) continue;
+                        const int c0 = __popc(m[u][0]);
+                        const bool b0 = (m[u][0] >> lane) & 1u, b1 = (m[u][1] >> lane) & 1u;
+                        const int r0 = __popc(m[u][0] & lanemask_lt());
+                        const int r1 = c0 + __popc(m[u][1] & lanemask_lt());
+                        // unconditional loads at rows clamped into the real (unpadded) plane
+                        const int hc0 = min(max(lane, g.pt), g.pt + g.H - 1);
+                        const int hc1 = min(max(32 + lane, g.pt), g.pt + g.H - 1);
+                        const float v0 = pl0[t[u].z + hc0 * g.W];
+                        const float v1 = pl0[t[u].z + hc1 * g.W];
+                        if (b0) dT[t[u].x + r0] = v0;
+                        if (b1) dT[t[u].x + r1] = v1;
+                        if (t[u].w & kTabIn) {
+                            const int Lc = t[u].w & 0xFFFF;
+                            if (b0) iT[t[u].y + r0] = Lc + lane * g.S;
+                            if (b1) iT[t[u].y + r1] = Lc + (32 + lane) * g.S;
+                        }
+                    }
+                }
+            } else {
+                for (int it = warp; it < nit; it += kEncWarps) {
+                    const int4 t = tab[it];
+                    if (!(t.w & kTabOk)) continue;
+                    int base = 0;
+                    for (int j = 0; j < NW; j++) {
+                        const unsigned m = msk[it * NW + j];
+                        if ((m >> lane) & 1u) {
+                            const int r = base + __popc(m & lanemask_lt());
+                            const int h = 32 * j + lane;
+                            dT[t.x + r] = pl0[t.z + h * g.W];
+                            if (t.w & kTabIn) iT[t.y + r] = (t.w & 0xFFFF) + h * g.S;
+                        }
+                        base += __popc(m);
+                    }
+                }
+            }
+        }
+        // ---- 7c. CPS IN of the overlapK_w columns: warp per column, lane per set4 group
+        if (CPS) {
+            for (int it = warp; it < np * Wp; it += kEncWarps) {
+                const int p = it / Wp, w = it % Wp;
+                if (!is_middle(g, w) || cnt[it] == 0 || !poff[4 * p + 3]) continue;
+                const int L = local_of(g, w);
+                int32_t* ii = a.in + poff[4 * p + 2] + inb[it];
+                const unsigned* mw = msk + it * NW;
+                int irun = 0;
+                for (int g0 = 0; g0 < 8 * NW; g0 += 32) {
+                    const int grp = g0 + lane;           // rows 4*grp .. 4*grp+3
+                    unsigned nib = 0;
+                    if (grp < 8 * NW) nib = (mw[grp >> 3] >> (4 * (grp & 7))) & 0xFu;
+                    const int k = __popc(nib);
+                    const int e = k >= 3 ? 2 : k;
                     int te;
                     const int eo = warp_exclusive_scan(e, &te);
-                    if (lane < 8 && k) {
-                        const int row0 = 32 * j + 4 * lane;
+                    if (k) {
+                        const int row0 = 4 * grp;
                         int32_t* o = ii + irun + eo;
                         if (k >= 3) {
                             o[0] = L + (row0 + __ffs(nib) - 1) * g.S;  // first NZE index (A9)
                             o[1] = (int32_t)nib;                         // pattern, bit b = row b (A12)
                         } else {
                             int u = 0;
-                            for (int b = 0; b < 4; b++)
-                                if ((nib >> b) & 1u) o[u++] = -(L + (row0 + b) * g.S);
+                            for (int bb = 0; bb < 4; bb++)
+                                if ((nib >> bb) & 1u) o[u++] = -(L + (row0 + bb) * g.S);
                         }
                     }
                     irun += te;
                 }
             }
         }
-        __syncthreads();   // the next tile reuses the shared memory
         probe(10);
+        fence_proxy_async();   // generic-proxy reads of this tile before the next bulk copy
+        __syncthreads();       // the next tile reuses the shared memory
+        probe(11);
     }
 }
 
@@ -432,7 +589,7 @@ int sm_count() {
 EncPlan plan_encode(const Geom& g) {
     EncPlan pl;
     const int sms = sm_count();
-    const size_t b2 = 100 * 1024, b1 = 220 * 1024;
+    const size_t b2 = 110 * 1024, b1 = 220 * 1024;
     long long P = (g.NC + 2 * sms - 1) / (2 * sms);
     if (enc_smem_layout(g, (int)P).total > b2) {
         P = (g.NC + sms - 1) / sms;
