@@ -327,11 +327,11 @@ struct ConvArgs {
 // all output rows (rt row tiles of TY rows, one per warp), KPL output channels
 // per lane (pairs (k, k+32) as float2 for FFMA2 when KPL is even), CH input
 // channels staged per chunk.
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2>
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8>
 struct StripCfg {
     static constexpr int MINB = MINB_;   // CTAs per SM targeted by the register budget
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
-    static constexpr int CH = 8, MAXW = 8, THREADS = 32 * MAXW;
+    static constexpr int MAXW = MAXW_, CH = MAXW_, THREADS = 32 * MAXW;   // warps; channels per chunk
     static constexpr int KB = 32 * KPL;               // output channels per CTA
     static constexpr int RS = R * S;
     static constexpr int NACC = KPL * TY * TX;        // accumulators per lane
@@ -355,6 +355,12 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ float4 lds128(const float4* p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
@@ -615,10 +621,13 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             // hierarchical walk: a warp-uniform branch skips each empty group of 4
             // consecutive window positions, then one per set position
             const float4* w4 = reinterpret_cast<const float4*>(win);
+            constexpr int NQ = (T::NCASE + 3) / 4;
+            float4 vn = lds128(w4);                      // prefetch: issued ahead of each skip branch
 #pragma unroll
-            for (int q = 0; q < (T::NCASE + 3) / 4; q++) {
+            for (int q = 0; q < NQ; q++) {
                 const unsigned nib = (mw[q >> 3] >> ((q & 7) * 4)) & 0xFu;
-                const float4 v4 = w4[q];
+                const float4 v4 = vn;
+                if (q + 1 < NQ) vn = lds128(w4 + q + 1);
                 if (nib) {
                     const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
@@ -637,7 +646,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 
     probe(5);
     // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
-    constexpr int TT = T::TY * T::TX, TP = TT + 1;
+    //      part = [RT*KB rows][TT positions], 16-byte chunks swizzled by (row & (NCH-1))
+    //      so the lane-per-row float4 stores and the chunk-per-thread reads are conflict-free
+    constexpr int TT = T::TY * T::TX, NCH = TT / 4;
+    static_assert(T::TX == 4 && (TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "tile layout");
     float accf[T::NACC];   // index kk*TT + t
 #pragma unroll
     for (int p = 0; p < T::NP; p++)
@@ -650,54 +662,72 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
             }
         }
-    float* part = s_w;   // [RT][KB][TP]: row tile, output channel (kk*32 + lane), position
+    float4* part4 = reinterpret_cast<float4*>(s_w);   // [RT*KB][NCH]
     if (CS > 1) {
-        float* red = part + RT * T::KB * TP;   // [CS-1][RT][NACC][32]
+        float4* red4 = part4 + RT * T::KB * NCH;       // [CS-1][RT][NACC/4][32]
         if (cs > 0) {
 #pragma unroll
-            for (int i = 0; i < T::NACC; i++) red[(((cs - 1) * RT + rtile) * T::NACC + i) * 32 + lane] = accf[i];
+            for (int i = 0; i < T::NACC / 4; i++)
+                red4[(((cs - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane] =
+                    make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
         }
         __syncthreads();
         if (cs == 0) {
+            for (int q = 1; q < CS; q++) {
 #pragma unroll
-            for (int i = 0; i < T::NACC; i++) {
-                float sum = accf[i];
-                for (int q = 1; q < CS; q++) sum += red[(((q - 1) * RT + rtile) * T::NACC + i) * 32 + lane];
-                part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = sum;
+                for (int i = 0; i < T::NACC / 4; i++) {
+                    const float4 v = red4[(((q - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane];
+                    accf[4 * i] += v.x; accf[4 * i + 1] += v.y; accf[4 * i + 2] += v.z; accf[4 * i + 3] += v.w;
+                }
             }
         }
-    } else {
+    }
+    if (cs == 0) {
 #pragma unroll
-        for (int i = 0; i < T::NACC; i++) part[(rtile * T::KB + (i / TT) * 32 + lane) * TP + i % TT] = accf[i];
+        for (int i = 0; i < T::NACC / 4; i++) {
+            const int row = rtile * T::KB + (i / NCH) * 32 + lane, c = i % NCH;
+            part4[row * NCH + (c ^ (row & (NCH - 1)))] =
+                make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+        }
     }
     probe(6);
     if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
     probe(7);
-    // ---- sum the cluster's partials (DSMEM), ReLU, store NKHW (t = ty*TX + tx fastest)
-    static_assert((TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "power-of-two tile and k block");
-    const int total = RT * T::KB * TT;
+    // ---- sum the cluster's partials (DSMEM, all peers' float4 loads in flight), ReLU,
+    //      NKHW store (a chunk = 4 consecutive output columns of one row)
+    const int total = RT * T::KB * NCH;
     const int per = (total + a.cg - 1) / a.cg;
     const int i0 = rank * per, i1 = min(total, i0 + per);
     float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
-    if (a.cg == 1) {
-        for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
-            const int t = i & (TT - 1), rk = i / TT, kl = rk & (T::KB - 1), rr = rk / T::KB;
-            const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + (t & (T::TX - 1));
-            float sum = part[rk * TP + t];
-            if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
+    const bool vec_ok = (g.Ow % 4) == 0;
+    auto cl = cgrp::this_cluster();
+    const float4* peer[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) peer[r] = (a.cg > 1 && r < a.cg) ? cl.map_shared_rank(part4, r) : part4;
+    for (int ci = i0 + threadIdx.x; ci < i1; ci += nthreads) {
+        const int row = ci / NCH, c = ci % NCH;
+        const int sidx = row * NCH + (c ^ (row & (NCH - 1)));
+        float4 v[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? peer[r][sidx] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 sum = v[0];
+#pragma unroll
+        for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
+        if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
+        const int kl = row & (T::KB - 1), rr = row / T::KB;
+        const int k = kbase + kl, oy = rr * T::TY + c;   // chunk c = output row c of the tile
+        if (k >= g.K || oy >= g.Oh) continue;
+        float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
+        if (vec_ok && ox0 + 3 < g.Ow) {
+            *reinterpret_cast<float4*>(dst) = sum;
+        } else {
+            const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (ox0 + q < g.Ow) dst[q] = sv[q];
         }
-    } else {
-        auto cl = cgrp::this_cluster();
-        for (int i = i0 + threadIdx.x; i < i1; i += nthreads) {
-            const int t = i & (TT - 1), rk = i / TT, kl = rk & (T::KB - 1), rr = rk / T::KB;
-            const int k = kbase + kl, oy = rr * T::TY + t / T::TX, ox = ox0 + (t & (T::TX - 1));
-            const int sidx = rk * TP + t;
-            float sum = 0.f;
-            for (int r = 0; r < a.cg; r++) sum += cl.map_shared_rank(part, r)[sidx];
-            if (k < g.K && oy < g.Oh && ox < g.Ow) yb[((long long)k * g.Oh + oy) * g.Ow + ox] = a.relu ? fmaxf(sum, 0.f) : sum;
-        }
-        cgrp::this_cluster().sync();
     }
+    if (a.cg > 1) cl.sync();
     probe(8);
 }
 
@@ -765,7 +795,7 @@ static size_t strip_smem(const ConvArgs& a) {
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
                         (size_t)T::CH * a.pmax * 4 + (size_t)T::CH * 4 + (size_t)T::MAXW * 64 * 4 + 16 +
                         (size_t)T::CH * 8;
-    const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX + 1) * 4 +
+    const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
 }
@@ -841,8 +871,8 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
     cudaError_t err = cudaErrorNotSupported;
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1>>(a, st);
-        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2>>(a, st);
+        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16>>(a, st);
+        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16>>(a, st);
         else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 1, 1, 4, 4, 4>>(a, st);
         else if (g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 4, 1>>(a, st);
     } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
