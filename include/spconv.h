@@ -140,6 +140,19 @@ spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, 
 spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const float *w_kcrs, float *y,
                                int32_t fuse_relu, void *ws_lowered, size_t ws_bytes, void *stream);
 
+/* GEMM engines of the dense baseline.  im2col_conv_forward uses the process-wide
+ * default (spc_set_im2col_gemm; initially SPC_GEMM_CUBLAS_FP32).  An engine the
+ * loaded cuBLAS lacks makes im2col_conv_forward return SPC_EUNSUPPORTED (BF16X9
+ * needs cuBLAS >= 12.9; PyTorch 2.11 bundles 12.8).  SPC_GEMM_SIMT is this library's own
+ * FP32 FFMA kernel; the cuBLAS engines are plain library GEMMs (cublasGemmStridedBatchedEx):
+ * FP32 = CUBLAS_COMPUTE_32F (FFMA), BF16X9 = CUBLAS_COMPUTE_32F_EMULATED_16BFX9
+ * (fp32 emulated with three bf16 terms on the tensor cores), TF32 =
+ * CUBLAS_COMPUTE_32F_FAST_TF32 (one tf32 term: faster, outside the 1e-4 tolerance;
+ * reported for the crossover only). */
+typedef enum { SPC_GEMM_SIMT = 0, SPC_GEMM_CUBLAS_FP32 = 1, SPC_GEMM_CUBLAS_BF16X9 = 2, SPC_GEMM_CUBLAS_TF32 = 3 } spc_gemm;
+spc_status spc_set_im2col_gemm(spc_gemm gemm);   /* SPC_EINVAL for an unknown engine */
+spc_gemm spc_get_im2col_gemm(void);
+
 /* Host, synchronising (it times).  Per-layer offline selection:
  * over the M sample maps (device, M*N*C*H*W fp32), time encode+conv for CPO
  * and CPS and lowering+GEMM for im2col, `reps` times each, sum per algorithm

@@ -71,12 +71,31 @@ _sigs = {
 for _n, _a in _sigs.items():
     getattr(_lib, _n).argtypes = _a
     getattr(_lib, _n).restype = ctypes.c_int
+_lib.spc_set_im2col_gemm.argtypes = [ctypes.c_int]
+_lib.spc_set_im2col_gemm.restype = ctypes.c_int
+_lib.spc_get_im2col_gemm.argtypes = []
+_lib.spc_get_im2col_gemm.restype = ctypes.c_int
 _lib.spc_select_ws_bytes.argtypes = [_D]
 _lib.spc_select_ws_bytes.restype = _sz
 _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
-EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version"]
+EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
+                          "spc_get_im2col_gemm"]
+SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32 = 0, 1, 2, 3
+GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
+              2: "cuBLAS FP32 emulated by 3 bf16 terms on tensor cores (CUBLAS_COMPUTE_32F_EMULATED_16BFX9)",
+              3: "cuBLAS TF32 tensor cores (CUBLAS_COMPUTE_32F_FAST_TF32, 1 term)"}
+
+
+def spc_set_im2col_gemm(gemm: int) -> None:
+    st = _lib.spc_set_im2col_gemm(int(gemm))
+    if st != SPC_OK:
+        raise SpcError(st, "spc_set_im2col_gemm")
+
+
+def spc_get_im2col_gemm() -> int:
+    return int(_lib.spc_get_im2col_gemm())
 
 
 def _check(rc: int, where: str):

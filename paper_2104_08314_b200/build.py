@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, probes: bool = False) -> s
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"])
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart", "-lcublas"])
     os.replace(lib + ".tmp", lib)
     return lib
 

@@ -180,8 +180,19 @@ spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const flo
     float* L = static_cast<float*>(ws_lowered);
     spc_status r = cuda_status(spc::launch_im2col(g, x, L, st), "im2col");
     if (r != SPC_OK) return r;
-    return cuda_status(spc::launch_gemm(g, w_kcrs, L, y, fuse_relu, st), "gemm");
+    const cudaError_t ge = spc::launch_gemm(g, w_kcrs, L, y, fuse_relu, st);
+    if (ge == cudaErrorNotSupported)
+        return fail(SPC_EUNSUPPORTED, "GEMM engine %d is not supported by the loaded cuBLAS", spc::gemm_engine());
+    return cuda_status(ge, "gemm");
 }
+
+spc_status spc_set_im2col_gemm(spc_gemm gemm) {
+    if (gemm < SPC_GEMM_SIMT || gemm > SPC_GEMM_CUBLAS_TF32) return fail(SPC_EINVAL, "unknown GEMM engine %d", (int)gemm);
+    spc::set_gemm_engine((int)gemm);
+    return SPC_OK;
+}
+
+spc_gemm spc_get_im2col_gemm(void) { return (spc_gemm)spc::gemm_engine(); }
 
 spc_status spc_encoding_lengths(const spc_encoding* enc, int64_t out_host[3], void* stream) {
     if (!enc || !enc->lengths || !out_host) return fail(SPC_EINVAL, "null pointer");

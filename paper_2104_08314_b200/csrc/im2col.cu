@@ -3,34 +3,61 @@
 // Lowering: L[n][c*R*S + l*S + m][y*Ow + x] = xp[n][c][y*sh + l][x*sw + m]
 // (SI Eq. 6 elements per image), written coalesced along the output position.
 // GEMM: y[n] (K x P) = W (K x CRS) * L[n] (CRS x P), P = Oh*Ow, FP32.
+#include <algorithm>
+#include <cublas_v2.h>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace spc {
 
-__global__ void im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ L) {
-    const long long P = (long long)g.Oh * g.Ow;
-    const long long RS = (long long)g.R * g.S;
-    const long long total = (long long)g.N * g.C * RS * P;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long p = i % P;
-        const long long row = i / P;           // n*CRS + crs
-        const long long crs = row % (g.C * RS);
-        const int n = (int)(row / (g.C * RS));
-        const int c = (int)(crs / RS);
-        const int l = (int)((crs % RS) / g.S), m = (int)(crs % g.S);
-        const int oy = (int)(p / g.Ow), ox = (int)(p % g.Ow);
+// Block (32, 8): threadIdx.x strides 32 consecutive output positions of a lowered row
+// (coalesced 128-byte stores), threadIdx.y picks one of 8 rows; rows = (n, c, l, m).
+__global__ void __launch_bounds__(256) im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ L) {
+    const int RS = g.R * g.S;
+    const long long rows = (long long)g.N * g.C * RS;
+    const int P = g.Oh * g.Ow;
+    const int p = blockIdx.x * 32 + threadIdx.x;
+    const int oy = p / g.Ow, ox = p - oy * g.Ow;
+    for (long long row = (long long)blockIdx.y * 8 + threadIdx.y; row < rows; row += (long long)gridDim.y * 8) {
+        const long long nc = row / RS;
+        const int rs = (int)(row - nc * RS);
+        const int l = rs / g.S, m = rs - l * g.S;
         const int h = oy * g.sh + l - g.pt, w = ox * g.sw + m - g.pl;
-        float v = 0.f;
-        if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(x + (((long long)n * g.C + c) * g.H + h) * g.W + w);
-        L[i] = v;
+        if (p < P)
+            L[row * P + p] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? __ldg(x + (nc * g.H + h) * g.W + w) : 0.f;
+    }
+}
+
+// Large Oh*Ow: one block row per lowered row, threads stride its positions.
+__global__ void __launch_bounds__(256) im2col_row_kernel(Geom g, const float* __restrict__ x, float* __restrict__ L) {
+    const int RS = g.R * g.S;
+    const long long row = blockIdx.y + (long long)blockIdx.z * gridDim.y;   // n*CRS + crs
+    const long long nc = row / RS;
+    const int rs = (int)(row - nc * RS);
+    const int l = rs / g.S, m = rs - l * g.S;
+    const int P = g.Oh * g.Ow;
+    const float* xc = x + nc * g.H * (long long)g.W;
+    float* Lr = L + row * P;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+        const int oy = p / g.Ow, ox = p - oy * g.Ow;
+        const int h = oy * g.sh + l - g.pt, w = ox * g.sw + m - g.pl;
+        Lr[p] = (h >= 0 && h < g.H && w >= 0 && w < g.W) ? __ldg(xc + h * g.W + w) : 0.f;
     }
 }
 
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st) {
-    long long total = (long long)g.N * g.C * g.R * g.S * g.Oh * g.Ow;
-    long long nb = (total + 255) / 256; int blocks = (int)(nb < 148 * 16 ? nb : 148 * 16);
-    im2col_kernel<<<blocks, 256, 0, st>>>(g, x, L);
+    const long long rows = (long long)g.N * g.C * g.R * g.S;
+    const int P = g.Oh * g.Ow;
+    if (P >= 512) {
+        long long rz = 1;
+        while ((rows + rz - 1) / rz > 65535 || rows % rz) rz++;
+        const int bx = std::min(8, (P + 255) / 256);
+        im2col_row_kernel<<<dim3(bx, (unsigned)(rows / rz), (unsigned)rz), 256, 0, st>>>(g, x, L);
+        return cudaGetLastError();
+    }
+    const long long ry = std::min<long long>((rows + 7) / 8, 65535);
+    im2col_kernel<<<dim3((P + 31) / 32, (unsigned)ry), dim3(32, 8), 0, st>>>(g, x, L);
     return cudaGetLastError();
 }
 
@@ -119,7 +146,57 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int Kd, const 
     }
 }
 
+__global__ void relu_kernel(float* y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = fmaxf(y[i], 0.f);
+}
+
+static int g_gemm = SPC_GEMM_CUBLAS_FP32;
+
+int gemm_engine() { return g_gemm; }
+void set_gemm_engine(int e) { g_gemm = e; }
+
+// one cuBLAS handle per device, created on first use (cuBLAS calls are stream-ordered
+// and capturable in CUDA graphs; the handle is only re-bound to the caller's stream)
+static cublasHandle_t cublas_handle(int dev) {
+    static std::mutex mu;
+    static cublasHandle_t h[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!h[dev] && cublasCreate(&h[dev]) != CUBLAS_STATUS_SUCCESS) h[dev] = nullptr;
+    return h[dev];
+}
+
+// y[n] (K x P, row-major) = W (K x CRS) * L[n] (CRS x P).  Column-major view for cuBLAS:
+// y^T (P x K, ld P) = L^T (P x CRS, ld P) * W^T (CRS x K, ld CRS), batched over n (W stride 0).
+static cudaError_t cublas_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
+                               int engine) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cublasHandle_t h = cublas_handle(dev);
+    if (!h) return cudaErrorNotSupported;
+    if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    const int P = g.Oh * g.Ow, K = g.K, CRS = g.C * g.R * g.S;
+    const float one = 1.f, zero = 0.f;
+    cublasComputeType_t ct = CUBLAS_COMPUTE_32F;
+    if (engine == SPC_GEMM_CUBLAS_BF16X9) ct = CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
+    if (engine == SPC_GEMM_CUBLAS_TF32) ct = CUBLAS_COMPUTE_32F_FAST_TF32;
+    cublasStatus_t s = cublasGemmStridedBatchedEx(
+        h, CUBLAS_OP_N, CUBLAS_OP_N, P, K, CRS, &one, L, CUDA_R_32F, P, (long long)CRS * P, w, CUDA_R_32F, CRS, 0,
+        &zero, y, CUDA_R_32F, P, (long long)K * P, g.N, ct, CUBLAS_GEMM_DEFAULT);
+    // the cuBLAS loaded in the process may predate an engine (BF16x9 needs cuBLAS >= 12.9;
+    // PyTorch bundles 12.8): report it as unsupported rather than as a CUDA fault
+    if (s == CUBLAS_STATUS_INVALID_VALUE || s == CUBLAS_STATUS_NOT_SUPPORTED) return cudaErrorNotSupported;
+    if (s != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    if (relu) {
+        const long long n = (long long)g.N * K * P;
+        relu_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, st>>>(y, n);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st) {
+    if (g_gemm != SPC_GEMM_SIMT) return cublas_gemm(g, w, L, y, relu, st, g_gemm);
     const int M = g.K, N = g.Oh * g.Ow, Kd = g.C * g.R * g.S;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, g.N);
     sgemm_kernel<<<grid, 256, 0, st>>>(M, N, Kd, w, L, (long long)Kd * N, y, (long long)M * N, relu);

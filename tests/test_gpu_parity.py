@@ -236,3 +236,45 @@ def test_select_layer_algo_argmin():
     wp = torch.from_numpy(he_normal(d["K"], d["C"], 1, 1, 1)).cuda()
     choice, t = spc.select_layer_algo(dp, samples, M, wp, spc.SPC_BEST_OF_THREE, 2, ws2)
     assert choice == spc.SPC_ALGO_IM2COL and t[1] == -1 and t[2] == -1
+
+
+@pytest.mark.parametrize("engine", [spc.SPC_GEMM_SIMT, spc.SPC_GEMM_CUBLAS_FP32, spc.SPC_GEMM_CUBLAS_BF16X9])
+def test_im2col_gemm_engines_within_tolerance(oracle_mod, engine):
+    """Every dense-baseline GEMM engine that the selector may use meets the fp32 tolerance."""
+    c = CONFIGS["cfg3"]
+    d = dict(c["desc"], N=2)
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], 0.3, c["seed"], c["dead_frac"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    ref = oracle_mod.direct_conv(d, x, w)
+    L = GpuLayer(d, w)
+    prev = spc.spc_get_im2col_gemm()
+    try:
+        spc.spc_set_im2col_gemm(engine)
+        try:
+            got = L.im2col(torch.from_numpy(x).cuda()).cpu().numpy()
+        except spc.SpcError as e:
+            if e.status == spc.SPC_EUNSUPPORTED:
+                pytest.skip(str(e))
+            raise
+        _check_conv(got, ref, f"gemm engine {spc.GEMM_NAMES[engine]}")
+        got_relu = L.im2col(torch.from_numpy(x).cuda(), relu=True).cpu().numpy()
+        _check_conv(got_relu, np.maximum(ref, 0.0), f"gemm engine {engine} + relu")
+    finally:
+        spc.spc_set_im2col_gemm(prev)
+
+
+def test_im2col_tf32_engine_runs():
+    """The 1-term TF32 engine is a crossover reference only: it must run, not meet 1e-4."""
+    d = layer_desc(1, 16, 14, 14, 16, 3, 3, 1, 1, 1, 1, 1, 1)
+    x = int_map(1, 16, 14, 14, 0.3, 5)
+    w = int_weights(16, 16, 3, 3, 5)
+    L = GpuLayer(d, w)
+    prev = spc.spc_get_im2col_gemm()
+    try:
+        spc.spc_set_im2col_gemm(spc.SPC_GEMM_CUBLAS_TF32)
+        got = L.im2col(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.isfinite(got).all()
+    finally:
+        spc.spc_set_im2col_gemm(prev)
+    with pytest.raises(spc.SpcError):
+        spc.spc_set_im2col_gemm(7)
