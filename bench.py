@@ -175,6 +175,94 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------- cfg5 stack leg
+
+def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
+    """cfg5: global batch args.stack_batch sharded over the ranks (strong scaling of this
+    sub-metric), per-layer plan selected offline on rank 0 and broadcast, the 16 layers
+    captured in one CUDA graph, then the one output gather (NCCL all-gather).
+    images/s = global batch / max over ranks of (stack + gather) device time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_08314_b200 as spc
+    from paper_2104_08314_b200.stack import Cfg5Stack, broadcast_plan, gather_outputs, shard_range
+    lo, hi = shard_range(args.stack_batch, world, rank)
+    S = Cfg5Stack(hi - lo, dev, rank=rank)
+    plan = S.select(args.stack_mode) if rank == 0 else None
+    plan = broadcast_plan(plan)
+    S.set_plan(plan)
+    graph = S.capture()
+    stream = torch.cuda.current_stream()
+    n_per_rank = [shard_range(args.stack_batch, world, r)[1] - shard_range(args.stack_batch, world, r)[0]
+                  for r in range(world)]
+    for _ in range(3):
+        graph.replay()
+        gather_outputs(S.layers[-1].y, n_per_rank)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.stack_steps)]
+    for i in range(args.stack_steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        graph.replay()
+        ev[i][1].record(stream)
+        out = gather_outputs(S.layers[-1].y, n_per_rank)
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    t_stack = sum(a.elapsed_time(b) for a, b, _ in ev) / args.stack_steps
+    t_gather = sum(b.elapsed_time(c) for _, b, c in ev) / args.stack_steps
+    tt = torch.tensor([t_stack, t_gather, t_stack + t_gather], device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_stack, t_gather, t_tot = (float(v) for v in tt.tolist())
+    assert out.shape[0] == args.stack_batch
+    # roofline of the chosen plan (per-layer t_roof = max(bytes / HBM, FLOPs / peak of its engine))
+    t_roof = 0.0
+    layers = []
+    for sp, L, algo, xb in zip(S.specs, S.layers, S.plan, S.host_inputs):
+        d = sp["desc"]
+        Oh, Ow = L.Oh, L.Ow
+        reps = (d["N"] + xb.shape[0] - 1) // xb.shape[0]
+        x_bytes = 4 * d["N"] * d["C"] * d["H"] * d["W"]
+        y_bytes = 4 * d["N"] * d["K"] * Oh * Ow
+        w_bytes = 4 * d["K"] * d["C"] * d["R"] * d["S"]
+        if algo == "im2col":
+            low = 4 * d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow
+            tr = max((x_bytes + 2 * low + w_bytes + y_bytes) / (hbm_gbs * 1e9),
+                     dense_flops(d, Oh, Ow) / (p_fp32 * 1e12))
+        else:
+            macs = nze_macs(dict(d, N=xb.shape[0]), xb, Oh, Ow) * reps * (d["N"] / (xb.shape[0] * reps))
+            nnz = int((xb != 0).sum()) * d["N"] / xb.shape[0]
+            enc_bytes = x_bytes + 8 * nnz + 8 * 3 * d["N"] * d["C"]
+            tr = max(enc_bytes / (hbm_gbs * 1e9), 0) + max((8 * nnz + w_bytes + y_bytes) / (hbm_gbs * 1e9),
+                                                          2.0 * macs / (p_fp32 * 1e12))
+        t_roof += tr
+        layers.append({"layer": sp["name"], "density": round(sp["density"], 4), "algo": algo})
+    res = {"workload": "cfg5 ResNet-50 3x3 stack (16 layers)", "global_batch": args.stack_batch,
+           "per_rank_batch": hi - lo, "n_gpus": world, "mode": args.stack_mode,
+           "images_per_s": args.stack_batch / (t_tot * 1e-3), "ms_per_step": t_tot, "stack_ms": t_stack,
+           "gather_ms": t_gather, "gather": "NCCL all_gather_into_tensor of the last layer's output" if world > 1
+           else "none (1 GPU)", "steps": args.stack_steps, "scaling": "strong (global batch fixed)",
+           "roofline_images_per_s": (hi - lo) / t_roof if t_roof > 0 else None,
+           "roofline_frac": (t_roof * 1e3) / t_tot if t_tot > 0 else None,
+           "plan": layers, "select_ms_per_sample": S.select_times if rank == 0 else None,
+           "gemm": spc.GEMM_NAMES[spc.spc_get_im2col_gemm()],
+           "inputs": "8 distinct seeded clustered-ReLU images per layer, tiled to the batch; L2 flushed per step"}
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        oracle.build()
+        t_cpu = 0.0
+        for sp, xb, w in zip(S.specs, S.host_inputs, S.weights):
+            t, n, _ = oracle_time(dict(sp["desc"], N=2), xb[:2], w, budget_s=1e9)
+            t_cpu += t
+        res["cpu_baseline"] = {"value": 2 / t_cpu, "unit": "images/s", "cores": 1, "kind": "oracle",
+                               "sample": "2 images through all 16 layers: oracle CPO encode + Alg. 2 conv, "
+                                         "single thread, FP64"}
+    return res
+
+
 # ---------------------------------------------------------------- GPU leg
 
 def run_ours(args):
@@ -321,6 +409,10 @@ def run_ours(args):
         cpu = {"value": f / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
                "sample": f"{n} image(s) of {args.workload}: oracle CPO encode + Alg. 2 conv, single thread, FP64"}
 
+    stack = None
+    if not args.no_stack:
+        stack = run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32)
+
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -337,7 +429,7 @@ def run_ours(args):
                          "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
                          "im2col_total": us(t_i2c)},
             "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
-                       "gemm": "SIMT FP32 FFMA (tile 128x128)"},
+                       "gemm": spc.GEMM_NAMES[spc.spc_get_im2col_gemm()]},
             "speedup_vs_im2col": t_i2c / t_ms,
             "cr": {"cpo": cr_cpo, "cps": cr_cps, "cpo_with_side_tables": s_im2col / (pl_ + dl_ + il_ + side),
                    "ptr": pl_, "da": dl_, "in_cpo": il_, "in_cps": is_, "S_im2col": s_im2col},
@@ -350,6 +442,7 @@ def run_ours(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "stack": stack,
             "version": spc.spc_version(),
         }
         print(json.dumps(line))
@@ -366,6 +459,10 @@ def main():
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stack", action="store_true", help="skip the cfg5 stack leg")
+    ap.add_argument("--stack-batch", type=int, default=256)
+    ap.add_argument("--stack-steps", type=int, default=10)
+    ap.add_argument("--stack-mode", default="best_of_three", choices=["favour_time", "favour_space", "best_of_three"])
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

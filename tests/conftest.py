@@ -10,6 +10,14 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
+    # the C-ABI library is git-ignored: build it (nvcc cross-compiles, no GPU needed) if absent
+    lib = os.path.join(ROOT, "paper_2104_08314_b200", "libspconv.so")
+    if not os.path.exists(lib):
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("_spc_build", os.path.join(ROOT, "paper_2104_08314_b200", "build.py"))
+        b = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(b)
+        b.build(force=True)
 
 
 @pytest.fixture(scope="session")
