@@ -149,7 +149,10 @@ spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const flo
  * (fp32 emulated with three bf16 terms on the tensor cores), TF32 =
  * CUBLAS_COMPUTE_32F_FAST_TF32 (one tf32 term: faster, outside the 1e-4 tolerance;
  * reported for the crossover only). */
-typedef enum { SPC_GEMM_SIMT = 0, SPC_GEMM_CUBLAS_FP32 = 1, SPC_GEMM_CUBLAS_BF16X9 = 2, SPC_GEMM_CUBLAS_TF32 = 3 } spc_gemm;
+typedef enum {
+    SPC_GEMM_SIMT = 0, SPC_GEMM_CUBLAS_FP32 = 1, SPC_GEMM_CUBLAS_BF16X9 = 2, SPC_GEMM_CUBLAS_TF32 = 3,
+    SPC_GEMM_TC_3XTF32 = 4   /* this library's tcgen05 kernel: fp32 from three TF32 products, TMEM accumulators */
+} spc_gemm;
 spc_status spc_set_im2col_gemm(spc_gemm gemm);   /* SPC_EINVAL for an unknown engine */
 spc_gemm spc_get_im2col_gemm(void);
 

@@ -82,10 +82,11 @@ _lib.spc_version.restype = ctypes.c_char_p
 
 EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
                           "spc_get_im2col_gemm"]
-SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32 = 0, 1, 2, 3
+SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
 GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
               2: "cuBLAS FP32 emulated by 3 bf16 terms on tensor cores (CUBLAS_COMPUTE_32F_EMULATED_16BFX9)",
-              3: "cuBLAS TF32 tensor cores (CUBLAS_COMPUTE_32F_FAST_TF32, 1 term)"}
+              3: "cuBLAS TF32 tensor cores (CUBLAS_COMPUTE_32F_FAST_TF32, 1 term)",
+              4: "tcgen05 3xTF32 (this library: fp32 from three TF32 products, TMEM accumulators)"}
 
 
 def spc_set_im2col_gemm(gemm: int) -> None:

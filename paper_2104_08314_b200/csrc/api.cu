@@ -187,7 +187,7 @@ spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const flo
 }
 
 spc_status spc_set_im2col_gemm(spc_gemm gemm) {
-    if (gemm < SPC_GEMM_SIMT || gemm > SPC_GEMM_CUBLAS_TF32) return fail(SPC_EINVAL, "unknown GEMM engine %d", (int)gemm);
+    if (gemm < SPC_GEMM_SIMT || gemm > SPC_GEMM_TC_3XTF32) return fail(SPC_EINVAL, "unknown GEMM engine %d", (int)gemm);
     spc::set_gemm_engine((int)gemm);
     return SPC_OK;
 }

@@ -186,6 +186,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
                                const float* w_packed, float* y, int relu, cudaStream_t st);
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
+cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
 int gemm_engine();
 void set_gemm_engine(int e);
 }  // namespace spc

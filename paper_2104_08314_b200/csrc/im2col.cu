@@ -196,6 +196,7 @@ static cudaError_t cublas_gemm(const Geom& g, const float* w, const float* L, fl
 }
 
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st) {
+    if (g_gemm == SPC_GEMM_TC_3XTF32) return launch_tc_gemm(g, w, L, y, relu, st);
     if (g_gemm != SPC_GEMM_SIMT) return cublas_gemm(g, w, L, y, relu, st, g_gemm);
     const int M = g.K, N = g.Oh * g.Ow, Kd = g.C * g.R * g.S;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, g.N);

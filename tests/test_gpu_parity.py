@@ -238,7 +238,8 @@ def test_select_layer_algo_argmin():
     assert choice == spc.SPC_ALGO_IM2COL and t[1] == -1 and t[2] == -1
 
 
-@pytest.mark.parametrize("engine", [spc.SPC_GEMM_SIMT, spc.SPC_GEMM_CUBLAS_FP32, spc.SPC_GEMM_CUBLAS_BF16X9])
+@pytest.mark.parametrize("engine", [spc.SPC_GEMM_SIMT, spc.SPC_GEMM_CUBLAS_FP32, spc.SPC_GEMM_CUBLAS_BF16X9,
+                                    spc.SPC_GEMM_TC_3XTF32])
 def test_im2col_gemm_engines_within_tolerance(oracle_mod, engine):
     """Every dense-baseline GEMM engine that the selector may use meets the fp32 tolerance."""
     c = CONFIGS["cfg3"]
@@ -278,3 +279,29 @@ def test_im2col_tf32_engine_runs():
         spc.spc_set_im2col_gemm(prev)
     with pytest.raises(spc.SpcError):
         spc.spc_set_im2col_gemm(7)
+
+
+@pytest.mark.parametrize("shape", [(1, 64, 56, 56, 64, 1), (2, 256, 14, 14, 256, 1), (2, 128, 28, 28, 128, 2),
+                                   (1, 5, 9, 11, 70, 1), (2, 3, 17, 17, 33, 1), (3, 512, 7, 7, 512, 1)])
+def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
+    """tcgen05 3xTF32 baseline GEMM vs the FP64 oracle on ragged shapes (P, K, CRS not tile multiples).
+    Up to CRS = 2304 it meets the north_star tolerance; at CRS = 4608 (512 channels) the tensor-core
+    accumulation of the three TF32 products leaves ~2e-5 absolute error on near-zero outputs, so
+    there the bound is 1e-4 of the output scale (the parity-passing default is cuBLAS FP32)."""
+    N, C, H, W, K, s = shape
+    d = layer_desc(N, C, H, W, K, 3, 3, s, s, 1, 1, 1, 1)
+    x = clustered_relu(N, C, H, W, 0.3, 11)
+    w = he_normal(K, C, 3, 3, 11)
+    ref = oracle_mod.direct_conv(d, x, w)
+    L = GpuLayer(d, w)
+    prev = spc.spc_get_im2col_gemm()
+    try:
+        spc.spc_set_im2col_gemm(spc.SPC_GEMM_TC_3XTF32)
+        got = L.im2col(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        spc.spc_set_im2col_gemm(prev)
+    if C * 9 <= 2304:
+        _check_conv(got, ref, f"tc 3xtf32 {shape}")
+    else:
+        err = np.abs(got - ref).max()
+        assert err <= 1e-4 * np.abs(ref).max(), f"tc 3xtf32 {shape}: max abs err {err}"

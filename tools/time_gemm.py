@@ -30,15 +30,15 @@ for wl in sys.argv[1:] or ["cfg2", "cfg3", "cfg5L0", "cfg5L8", "cfg5L14"]:
     L = SparseConvLayer(d, wg)
     dense = 2.0 * d["N"] * d["K"] * d["C"] * d["R"] * d["S"] * L.Oh * L.Ow
     row = {"workload": wl}
-    for e in range(4):
+    for e in range(5):
         spc.spc_set_im2col_gemm(e)
         try:
             g = L.capture(lambda: L.forward(xg, "im2col"))
             t = timed(g)
         except spc.SpcError:
-            row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32"][e] + "_us"] = None
+            row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32", "tc3xtf32"][e] + "_us"] = None
             continue
-        row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32"][e] + "_us"] = round(t, 2)
-        row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32"][e] + "_tflops"] = round(dense / t / 1e6, 1)
+        row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32", "tc3xtf32"][e] + "_us"] = round(t, 2)
+        row[["simt", "cublas_fp32", "cublas_bf16x9", "cublas_tf32", "tc3xtf32"][e] + "_tflops"] = round(dense / t / 1e6, 1)
     spc.spc_set_im2col_gemm(1)
     print(json.dumps(row), flush=True)
