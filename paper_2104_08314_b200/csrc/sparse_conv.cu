@@ -682,6 +682,42 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
     }
+    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
+    const bool vec_ok = (g.Ow % 4) == 0;
+    if (a.cg == 1) {
+        // no cluster split: store straight from registers (a lane owns output channel
+        // kk*32+lane and a 4-wide output row per accumulator chunk).  With a cluster split
+        // the DSMEM reduction below wins: measured, red.global.add.v4 of every rank's
+        // partial costs 8x the transactions and is slower at cfg2/cfg3.
+        auto emit = [&](bool add) {
+#pragma unroll
+            for (int i = 0; i < T::NACC / 4; i++) {
+                const int k = kbase + (i / NCH) * 32 + lane, oy = rtile * T::TY + (i % NCH);
+                if (k >= g.K || oy >= g.Oh) continue;
+                float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+                if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+                float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
+                if (vec_ok && ox0 + 3 < g.Ow) {
+                    if (add)
+                        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                                     ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+                    else
+                        *reinterpret_cast<float4*>(dst) = v;
+                } else {
+                    const float sv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (ox0 + q < g.Ow) {
+                            if (add) atomicAdd(dst + q, sv[q]);
+                            else dst[q] = sv[q];
+                        }
+                }
+            }
+        };
+        if (cs == 0) emit(false);
+        probe(8);
+        return;
+    }
     if (cs == 0) {
 #pragma unroll
         for (int i = 0; i < T::NACC / 4; i++) {
@@ -698,8 +734,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     const int total = RT * T::KB * NCH;
     const int per = (total + a.cg - 1) / a.cg;
     const int i0 = rank * per, i1 = min(total, i0 + per);
-    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
-    const bool vec_ok = (g.Ow % 4) == 0;
     auto cl = cgrp::this_cluster();
     const float4* peer[8];
 #pragma unroll
@@ -727,6 +761,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 if (ox0 + q < g.Ow) dst[q] = sv[q];
         }
     }
+    probe(9);
     if (a.cg > 1) cl.sync();
     probe(8);
 }

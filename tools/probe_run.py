@@ -52,7 +52,8 @@ for wl in sys.argv[1:] or ["cfg1", "cfg2"]:
         L.forward(xg, "cpo")
     torch.cuda.synchronize()
     grab(lib.spc_debug_probes_enc); grab(lib.spc_debug_probes_conv)
-    flush.zero_()
+    if not os.environ.get("PROBE_NOFLUSH"):
+        flush.zero_()
     L.forward(xg, "cpo")
     torch.cuda.synchronize()
     e, cv = grab(lib.spc_debug_probes_enc), grab(lib.spc_debug_probes_conv)
