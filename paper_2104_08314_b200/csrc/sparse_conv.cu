@@ -327,11 +327,12 @@ struct ConvArgs {
 // all output rows (rt row tiles of TY rows, one per warp), KPL output channels
 // per lane (pairs (k, k+32) as float2 for FFMA2 when KPL is even), CH input
 // channels staged per chunk.
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8>
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8, int CH_ = 16>
 struct StripCfg {
     static constexpr int MINB = MINB_;   // CTAs per SM targeted by the register budget
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
-    static constexpr int MAXW = MAXW_, CH = MAXW_, THREADS = 32 * MAXW;   // warps; channels per chunk
+    static constexpr int MAXW = MAXW_, THREADS = 32 * MAXW;
+    static constexpr int CH = CH_;        // input channels staged per chunk (fewer chunk barriers when larger)
     static constexpr int KB = 32 * KPL;               // output channels per CTA
     static constexpr int RS = R * S;
     static constexpr int NACC = KPL * TY * TX;        // accumulators per lane
@@ -497,7 +498,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
     const bool w16 = (g.K % 4) == 0;
 
-    const int CHS = min(T::CH, nwarps);       // channels per chunk: one per warp in P1
+    // channels per chunk (P1: warps stride the channels); a chunk slightly larger than the
+    // warp count would leave one warp doing two channels' scatter, so trim it then
+    const int CHS = (T::CH % nwarps == 0 || T::CH >= 2 * nwarps) ? T::CH : min(T::CH, nwarps);
     // taps W[c][l][m][kbase..+KB) of a chunk -> s_w (cp.async); independent of the encoding
     auto stage_w = [&](int c0, int chn) {
         const float* wsrc = a.wp + (long long)c0 * T::RS * g.K + kbase;   // row (j*RS+rs) at stride K
@@ -906,13 +909,13 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
     cudaError_t err = cudaErrorNotSupported;
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16>>(a, st);
-        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16>>(a, st);
+        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16, 32>>(a, st);
+        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32>>(a, st);
         else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 1, 1, 4, 4, 4>>(a, st);
         else if (g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 4, 1>>(a, st);
     } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
         if (g.K <= 64 && g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 2>>(a, st);
-        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4>>(a, st);
+        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>>(a, st);   // 8: keeps 2 CTAs/SM
     } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
         err = run_strip<StripCfg<1, 7, 1, 1, 8, 4, 2>>(a, st);
     } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
