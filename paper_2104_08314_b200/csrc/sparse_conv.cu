@@ -915,6 +915,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         else if (g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 4, 1>>(a, st);
     } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
         if (g.K <= 64 && g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 2>>(a, st);
+        else if (g.Oh <= 16) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>>(a, st);
         else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>>(a, st);   // 8: keeps 2 CTAs/SM
     } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
         err = run_strip<StripCfg<1, 7, 1, 1, 8, 4, 2>>(a, st);
