@@ -373,12 +373,12 @@ def run_ours(args):
             traffic = None
     if conv_s >= enc_s:
         if conv_bound == "alu":
-            roof = {"kernel": "sparse_conv_kernel", "bound": "alu", "achieved": conv_flops / conv_s / 1e12,
+            roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "alu", "achieved": conv_flops / conv_s / 1e12,
                     "peak": p_fp32, "unit": "TFLOP/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
                     "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
                     "algorithmic_flops": conv_flops, "algorithmic_bytes": conv_bytes}
         else:
-            roof = {"kernel": "sparse_conv_kernel", "bound": "hbm", "achieved": conv_bytes / conv_s / 1e9,
+            roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "hbm", "achieved": conv_bytes / conv_s / 1e9,
                     "peak": hbm_gbs, "unit": "GB/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
                     "peak_source": peak_src, "algorithmic_bytes": conv_bytes}
     else:

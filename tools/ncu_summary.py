@@ -13,7 +13,7 @@ import subprocess
 import sys
 
 KEYS = [
-    ("gpu__time_duration.sum", "duration_ns"),
+    ("gpu__time_duration.sum", "duration_us"),
     ("dram__bytes_read.sum", "dram_read_B"),
     ("dram__bytes_write.sum", "dram_write_B"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
