@@ -37,6 +37,7 @@ from synth import CONFIGS, cfg5_layers, clustered_relu, he_normal  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT, FP32_LANES, FALLBACK_HBM = 148, 128, 6650.0
+METRIC = "dense-equivalent GFLOP/s of CPO encode + sparse conv (per layer), vs GPU im2col"
 
 
 def workload(name: str):
@@ -164,7 +165,7 @@ def run_reference(args):
         t, n, f = oracle_time(d, x, w, budget_s=20.0 / max(1, args.steps))
         tot_t, tot_f, imgs = tot_t + t, tot_f + f, imgs + n
     val = tot_f / tot_t / 1e9
-    line = {"impl": "reference", "metric": "dense-equivalent GFLOP/s of CPO encode + sparse conv (per layer)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -418,7 +419,7 @@ def run_ours(args):
     if rank == 0:
         us = lambda ms: 1e3 * ms / args.steps  # noqa: E731
         line = {
-            "metric": "dense-equivalent GFLOP/s of CPO encode + sparse conv (per layer), vs GPU im2col",
+            "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
