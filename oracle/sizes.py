@@ -78,3 +78,41 @@ def channel_density(x: np.ndarray) -> np.ndarray:
     """rho_{n,c}: fraction of NZEs in each channel plane."""
     N, C, H, W = x.shape
     return (x.reshape(N, C, H * W) != 0).sum(axis=2) / float(H * W)
+
+
+# ---- SI space-complexity bounds (PAPER.md:590-689), written out as printed ----------
+#
+# Reading A29 (DESIGN.md): the printed P(rho) bounds the SUM of the channel densities
+# with a factor I_n I_c, then clips it to [0, 1]; only the average channel density
+# rho_bar = sum_{n,c} rho_{n,c} / (I_n I_c) makes the clip meaningful, so the bound is
+# taken on rho_bar:  rho_bar <= B / (I_n I_c).  Worst case as stated: M = 1 (VALID),
+# no NPC, no NPF, K_w > s_w; ceil(K_w / s_w) = K_w for the stride-agnostic encoding (A15).
+
+def _kw_ceil(d: dict) -> int:
+    return d["S"]
+
+
+def p_bound_im2col(d: dict) -> float:
+    """Average density below which S_CPO <= S_im2col:
+    (O_w (K_w K_h O_h + 1 - ceil(K_w/s_w)) - 2 - ceil(K_w/s_w)) / (2 I_h I_w), in [0, 1].
+    O_w, O_h here are the stride-1 partition counts of the encoding (A15)."""
+    ow, oh = _ow1(d), d["H"] + d["pad_top"] + d["pad_bottom"] - d["R"] + 1
+    kc = _kw_ceil(d)
+    b = (ow * (d["S"] * d["R"] * oh + 1 - kc) - 2 - kc) / (2.0 * d["H"] * d["W"])
+    return min(1.0, max(0.0, b))
+
+
+def p_bound_mec(d: dict) -> float:
+    """Average density below which S_CPO <= S_MEC:
+    (O_w (K_w I_h + 1 - ceil(K_w/s_w)) - 2 - ceil(K_w/s_w)) / (2 I_h I_w), in [0, 1]."""
+    ow = _ow1(d)
+    kc = _kw_ceil(d)
+    b = (ow * (d["S"] * d["H"] + 1 - kc) - 2 - kc) / (2.0 * d["H"] * d["W"])
+    return min(1.0, max(0.0, b))
+
+
+def s_cpo_worst(d: dict, rho_bar: float) -> float:
+    """Worst-case CPO size of the derivation:
+    I_n I_c (3 + (ceil(K_w/s_w) - 1)(1 + O_w)) + 2 I_h I_w sum rho."""
+    ow = _ow1(d)
+    return d["N"] * d["C"] * (3 + (_kw_ceil(d) - 1) * (1 + ow)) + 2 * d["H"] * d["W"] * d["N"] * d["C"] * rho_bar

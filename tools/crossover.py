@@ -30,6 +30,7 @@ def main():
 
     import paper_2104_08314_b200 as spc
     from bench import workload
+    from paper_2104_08314_b200.bounds import rho_space_bound
     from paper_2104_08314_b200.layer import SparseConvLayer
     from synth import clustered_relu, he_normal
 
@@ -68,14 +69,20 @@ def main():
             t_dense[name] = timed(L.capture(lambda: L.forward(x0, "im2col")))
         spc.spc_set_im2col_gemm(spc.SPC_GEMM_CUBLAS_FP32)
         rows = []
+        s_i2c = d["N"] * L.Oh * L.Ow * d["C"] * d["R"] * d["S"]
         for rho in RHOS:
             # the config's dead channels / zero tiles cap the reachable density: keep them
             # up to rho = 0.5, plain clustered maps above
             dead, zt = (c["dead_frac"], c["zero_tile_frac"]) if rho <= 0.5 else (0.0, 0.0)
             x = torch.from_numpy(clustered_relu(d["N"], d["C"], d["H"], d["W"], rho, c["seed"], dead, zt)).cuda()
             t_cpo = timed(L.capture(lambda: L.forward(x, "cpo")))
+            L.forward(x, "cpo")
+            cr_cpo = s_i2c / sum(L.lengths())
             t_cps = timed(L.capture(lambda: L.forward(x, "cps")))
-            rows.append({"rho": rho, "cpo_us": round(t_cpo, 2), "cps_us": round(t_cps, 2)})
+            L.forward(x, "cps")
+            cr_cps = s_i2c / sum(L.lengths())
+            rows.append({"rho": rho, "cpo_us": round(t_cpo, 2), "cps_us": round(t_cps, 2),
+                         "cr_cpo": round(cr_cpo, 3), "cr_cps": round(cr_cps, 3)})
 
         def crossing(key, ref):
             for a, b in zip(rows, rows[1:]):
@@ -87,9 +94,18 @@ def main():
                "im2col_us": {k: round(v, 2) for k, v in t_dense.items()}, "sweep": rows,
                "crossover_rho": {f"cpo_vs_{k}": crossing("cpo_us", v) for k, v in t_dense.items()}}
         res["crossover_rho"].update({f"cps_vs_{k}": crossing("cps_us", v) for k, v in t_dense.items()})
+
+        def cr_one(key):   # first density where the encoding stops being smaller than S_im2col
+            for a, b in zip(rows, rows[1:]):
+                if a[key] >= 1.0 > b[key]:
+                    return round(a["rho"] + (b["rho"] - a["rho"]) * (a[key] - 1.0) / (a[key] - b[key]), 3)
+            return ">1.0" if rows[-1][key] >= 1.0 else None
+        # SI P(rho) (worst case: VALID, no NPC/NPF) must not exceed the measured CR = 1 density
+        res["space"] = {"p_bound_rho_im2col": round(rho_space_bound(d, "im2col"), 4),
+                        "measured_cr1_rho_cpo": cr_one("cr_cpo"), "measured_cr1_rho_cps": cr_one("cr_cps")}
         results.append(res)
-        print(json.dumps({"workload": wl, "im2col_us": res["im2col_us"], "crossover_rho": res["crossover_rho"]}),
-              flush=True)
+        print(json.dumps({"workload": wl, "im2col_us": res["im2col_us"], "crossover_rho": res["crossover_rho"],
+                          "space": res["space"]}), flush=True)
         del L
         torch.cuda.empty_cache()
     if args.out:
