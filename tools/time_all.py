@@ -2,7 +2,7 @@
 """Device time of encode and conv (CPO) per workload, auto tile config, in one process.
 
   python tools/time_all.py [workload ...]
-Prints one JSON line per workload (CUDA graph replay, L2 flushed between reps, median).
+Prints one JSON line per workload (CUDA graph replay, L2 flushed between reps, mean of 200).
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ def main():
     from paper_2104_08314_b200.layer import SparseConvLayer
     flush = torch.empty(64 * 2 ** 20, device="cuda")
 
-    def timed(gr, n=50):
+    def timed(gr, n=200):
         for _ in range(3):
             gr.replay()
         torch.cuda.synchronize()
@@ -32,8 +32,10 @@ def main():
             flush.zero_()
             a.record(); gr.replay(); b.record()
         torch.cuda.synchronize()
-        ts = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
-        return ts[len(ts) // 2]
+        # event resolution is 32 ns (tools/microbench/event_resolution.py), but step times on
+        # this pool cluster at multiples of ~2.05 us (launch scheduling): report the mean
+        ts = [a.elapsed_time(b) * 1e3 for a, b in ev]
+        return sum(ts) / len(ts)
 
     for wl in (sys.argv[1:] or WORKLOADS):
         c = workload(wl)
