@@ -138,6 +138,18 @@ def test_cfg5_layers_sampled(oracle_mod, li):
     _layer_case(oracle_mod, d, x, w, full=False, samples=3000, seed=li)
 
 
+@pytest.mark.parametrize("shape", [(48, 64, 56, 56), (96, 128, 28, 28)])
+def test_encoder_multi_round_tiles(oracle_mod, shape):
+    """Batches whose tiles outnumber the resident CTAs (the cfg5 stack at batch 256 on one
+    GPU): the encoder's persistent multi-round path must still emit the oracle's streams
+    bit for bit, and the conv must stay within tolerance on sampled outputs."""
+    N, C, H, W = shape
+    d = layer_desc(N, C, H, W, C, 3, 3, 1, 1, 1, 1, 1, 1)
+    x = clustered_relu(N, C, H, W, 0.25, 77)
+    w = he_normal(C, C, 3, 3, 77)
+    _layer_case(oracle_mod, d, x, w, full=False, samples=2000, seed=5)
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _desc3(**kw):
