@@ -130,7 +130,8 @@ spc_status spc_pack_weights(const spc_conv_desc *d, const float *w_kcrs, float *
  * with any stride (reading A15, DESIGN.md A.7).  All-zero channels (NPC) and
  * regions (NPF) are skipped.  fuse_relu != 0 applies max(0, .) to y.
  * For a CPS encoding the pattern sets are expanded into ws first.
- * ws: >= ws_bytes from spc_encode_capacity (may be NULL for CPO). */
+ * ws: >= ws_bytes from spc_encode_capacity (may be NULL for CPO; with it, a cluster-split
+ * launch reduces its partial sums through L2 instead of distributed shared memory). */
 spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
                                float *y, int32_t fuse_relu, void *ws, size_t ws_bytes, void *stream);
 

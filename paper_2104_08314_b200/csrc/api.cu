@@ -165,7 +165,17 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
         if (r != SPC_OK) return r;
         in_cpo = buf;
     }
-    return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, st), "sparse_conv");
+    float* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    if (ws) {
+        const spc::WsLayout L = spc::ws_layout(g);
+        if (ws_bytes >= L.total && L.total > L.scratch) {
+            scratch = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + L.scratch);
+            scratch_bytes = L.total - L.scratch;
+        }
+    }
+    return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, scratch, scratch_bytes, st),
+                       "sparse_conv");
 }
 
 spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const float* w_kcrs, float* y,

@@ -53,9 +53,11 @@ __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a -
 // upper bound on encoder tiles (one plane per tile), for workspace sizing
 inline long long enc_tiles(const Geom& g) { return g.NC; }
 
-// Workspace layout: [EncState | flags[ntiles] (u64) | agg[3*ntiles] | cps_in[da_cap]]
+size_t conv_scratch_bytes(const Geom& g);   // sparse_conv.cu: L2 partials of a cluster split
+
+// Workspace layout: [EncState | flags[ntiles] (u64) | agg[3*ntiles] | cps_in[da_cap] | conv partials]
 struct WsLayout {
-    size_t state, flags, agg, cps_in, total;
+    size_t state, flags, agg, cps_in, scratch, total;
 };
 
 inline WsLayout ws_layout(const Geom& g) {
@@ -65,7 +67,8 @@ inline WsLayout ws_layout(const Geom& g) {
     L.flags = align_up(sizeof(EncState), 256);
     L.agg = align_up(L.flags + sizeof(unsigned long long) * (size_t)nt, 256);
     L.cps_in = align_up(L.agg + sizeof(long long) * 3 * (size_t)nt, 256);
-    L.total = align_up(L.cps_in + sizeof(int32_t) * (size_t)(g.NC * g.H * g.W), 256);
+    L.scratch = align_up(L.cps_in + sizeof(int32_t) * (size_t)(g.NC * g.H * g.W), 256);
+    L.total = align_up(L.scratch + conv_scratch_bytes(g), 256);
     return L;
 }
 
@@ -183,7 +186,8 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
 cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaStream_t st);
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st);
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
-                               const float* w_packed, float* y, int relu, cudaStream_t st);
+                               const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
+                               cudaStream_t st);
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
 cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);

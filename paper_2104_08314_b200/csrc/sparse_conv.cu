@@ -321,6 +321,8 @@ struct ConvArgs {
     int pmax;       // longest ptr segment of one channel
     int rt;         // strip kernel: row tiles per strip (warps per channel split)
     int csplit;     // strip kernel: channel splits inside the CTA
+    float* scratch; // strip kernel, cg > 1: per-CTA partials for the L2 cluster reduction (or null)
+    size_t scratch_bytes;
 };
 
 // Strip-kernel configuration: a CTA owns a column strip of TX output columns and
@@ -666,6 +668,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
     float4* part4 = reinterpret_cast<float4*>(s_w);   // [RT*KB][NCH]
+    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
+    const bool vec_ok = (g.Ow % 4) == 0;
     if (CS > 1) {
         float4* red4 = part4 + RT * T::KB * NCH;       // [CS-1][RT][NACC/4][32]
         if (cs > 0) {
@@ -685,8 +689,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
     }
-    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
-    const bool vec_ok = (g.Ow % 4) == 0;
     if (a.cg == 1) {
         // no cluster split: store straight from registers (a lane owns output channel
         // kk*32+lane and a 4-wide output row per accumulator chunk).  With a cluster split
@@ -718,6 +720,55 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         };
         if (cs == 0) emit(false);
+        probe(8);
+        return;
+    }
+    if (a.scratch) {
+        // cluster split, reduced through L2: each CTA stores its partial ([NCH][RT*KB] float4,
+        // coalesced along rows), one cluster barrier (release / acquire) publishes them, then
+        // each rank sums its share of the chunks over the cg partials (L2 reads, all peers'
+        // loads in flight).  Measured: DSMEM moves this traffic ~10x slower on this part
+        // (tools/microbench/dsmem.cu).
+        const int rows = RT * T::KB;
+        const long long slot0 = ((long long)(blockIdx.z - rank) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const long long sstride = (long long)gridDim.y * gridDim.x;       // next cluster rank
+        float4* mine = reinterpret_cast<float4*>(a.scratch) + (slot0 + rank * sstride) * (long long)rows * NCH;
+        if (cs == 0) {
+#pragma unroll
+            for (int i = 0; i < T::NACC / 4; i++) {
+                const int row = rtile * T::KB + (i / NCH) * 32 + lane, c = i % NCH;
+                mine[(long long)c * rows + row] = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+            }
+        }
+        probe(6);
+        cgrp::this_cluster().sync();
+        probe(7);
+        const int total = rows * NCH;
+        const int per = (total + a.cg - 1) / a.cg;
+        const float4* base = reinterpret_cast<const float4*>(a.scratch) + slot0 * (long long)rows * NCH;
+        const long long pstride = sstride * (long long)rows * NCH;
+        for (int ci = rank * per + threadIdx.x; ci < min(total, (rank + 1) * per); ci += nthreads) {
+            float4 v[8];
+#pragma unroll
+            for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? __ldcg(base + r * pstride + ci) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 sum = v[0];
+#pragma unroll
+            for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
+            if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
+            const int c = ci / rows, row = ci % rows;
+            const int k = kbase + (row & (T::KB - 1)), oy = (row / T::KB) * T::TY + c;
+            if (k >= g.K || oy >= g.Oh) continue;
+            float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
+            if (vec_ok && ox0 + 3 < g.Ow) {
+                *reinterpret_cast<float4*>(dst) = sum;
+            } else {
+                const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (ox0 + q < g.Ow) dst[q] = sv[q];
+            }
+        }
+        probe(9);
         probe(8);
         return;
     }
@@ -853,18 +904,38 @@ static int tune_cg() {
     return env ? atoi(env) : 0;
 }
 
+// The launch geometry of a strip config: strips, k-blocks, row tiles, cluster split.
+template <class T>
+struct StripPlan {
+    int strips, kblocks, rt, csplit, cg;
+    long long ctas;
+    size_t scratch_bytes;   // L2 partials when cg > 1
+};
+template <class T>
+static StripPlan<T> plan_strip(const Geom& g) {
+    StripPlan<T> p;
+    p.strips = (g.Ow + T::TX - 1) / T::TX;
+    p.rt = (g.Oh + T::TY - 1) / T::TY;
+    p.csplit = std::max(1, T::MAXW / std::max(1, p.rt));
+    p.kblocks = (g.K + T::KB - 1) / T::KB;
+    p.ctas = (long long)p.strips * p.kblocks * g.N;
+    int cg = tune_cg();
+    if (cg <= 0) cg = pick_cg(p.ctas, g.C, T::MINB);
+    p.cg = cg;
+    p.scratch_bytes = (cg > 1) ? (size_t)p.ctas * cg * p.rt * T::KB * (T::TY * T::TX) * sizeof(float) : 0;
+    return p;
+}
+
 template <class T>
 static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
-    const int strips = (g.Ow + T::TX - 1) / T::TX;
-    a.rt = (g.Oh + T::TY - 1) / T::TY;
+    const StripPlan<T> pl = plan_strip<T>(g);
+    const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
+    a.rt = pl.rt;
     if (a.rt > T::MAXW) return cudaErrorInvalidValue;
-    a.csplit = std::max(1, T::MAXW / a.rt);
-    const int kblocks = (g.K + T::KB - 1) / T::KB;
-    const long long ctas = (long long)strips * kblocks * g.N;
-    int cg = tune_cg();
-    if (cg <= 0) cg = pick_cg(ctas, g.C, T::MINB);
+    a.csplit = pl.csplit;
     a.cg = cg;
+    if (cg <= 1 || a.scratch_bytes < pl.scratch_bytes) a.scratch = nullptr;
     const size_t smem = strip_smem<T>(a);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static size_t attr_bytes = 0;     // per instantiation
@@ -890,8 +961,39 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T>, a);
 }
 
+// Calls f(StripCfg<...>{}) for the strip configuration of this geometry; returns
+// cudaErrorNotSupported when none applies (the generic kernel runs instead).
+template <class F>
+static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
+    if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
+        if (g.K <= 32 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16, 32>{});
+        if (g.K <= 64 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32>{});
+        if (g.Oh <= 32) return f(StripCfg<3, 3, 1, 1, 4, 4, 4>{});
+        if (g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 4, 1>{});
+    } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
+        if (g.K <= 64 && g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 2>{});
+        if (g.Oh <= 16) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>{});
+        if (g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>{});   // 8: keeps 2 CTAs/SM
+    } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
+        return f(StripCfg<1, 7, 1, 1, 8, 4, 2>{});
+    } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
+        return f(StripCfg<7, 1, 1, 1, 8, 4, 2>{});
+    }
+    return cudaErrorNotSupported;
+}
+
+size_t conv_scratch_bytes(const Geom& g) {
+    size_t bytes = 0;
+    visit_strip_cfg(g, [&](auto cfg) {
+        bytes = plan_strip<decltype(cfg)>(g).scratch_bytes;
+        return cudaSuccess;
+    });
+    return bytes;
+}
+
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
-                               const float* w_packed, float* y, int relu, cudaStream_t st) {
+                               const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
+                               cudaStream_t st) {
     ConvArgs a;
     a.g = g;
     a.ptr = e->ptr;
@@ -906,22 +1008,10 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.cg = 1;
     a.rt = 1;
     a.csplit = 1;
+    a.scratch = scratch;
+    a.scratch_bytes = scratch_bytes;
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
-    cudaError_t err = cudaErrorNotSupported;
-    if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
-        if (g.K <= 32 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16, 32>>(a, st);
-        else if (g.K <= 64 && g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32>>(a, st);
-        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 1, 1, 4, 4, 4>>(a, st);
-        else if (g.Oh <= 64) err = run_strip<StripCfg<3, 3, 1, 1, 8, 4, 4, 1>>(a, st);
-    } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
-        if (g.K <= 64 && g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 2>>(a, st);
-        else if (g.Oh <= 16) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>>(a, st);
-        else if (g.Oh <= 32) err = run_strip<StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>>(a, st);   // 8: keeps 2 CTAs/SM
-    } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
-        err = run_strip<StripCfg<1, 7, 1, 1, 8, 4, 2>>(a, st);
-    } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
-        err = run_strip<StripCfg<7, 1, 1, 1, 8, 4, 2>>(a, st);
-    }
+    cudaError_t err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;

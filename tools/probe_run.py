@@ -52,9 +52,17 @@ for wl in sys.argv[1:] or ["cfg1", "cfg2"]:
         L.forward(xg, "cpo")
     torch.cuda.synchronize()
     grab(lib.spc_debug_probes_enc); grab(lib.spc_debug_probes_conv)
+    if os.environ.get("PROBE_GRAPH"):
+        gr = L.capture(lambda: L.forward(xg, "cpo"))
+        gr.replay()
+        torch.cuda.synchronize()
+        grab(lib.spc_debug_probes_enc); grab(lib.spc_debug_probes_conv)
     if not os.environ.get("PROBE_NOFLUSH"):
         flush.zero_()
-    L.forward(xg, "cpo")
+    if os.environ.get("PROBE_GRAPH"):
+        gr.replay()
+    else:
+        L.forward(xg, "cpo")
     torch.cuda.synchronize()
     e, cv = grab(lib.spc_debug_probes_enc), grab(lib.spc_debug_probes_conv)
     print(f"== {wl}")
