@@ -254,36 +254,48 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
     const int S = g.S;
     int q = dmid, dpos = dmid;
     bool carry_pat = false;  // next entry is a pattern (its index ended the previous chunk)
+    constexpr int B = 8;     // chunks of 32 entries whose loads are in flight together
     while (q < nin) {
-        const int i = q + lane;
-        const bool valid = i < nin;
-        const int e = valid ? __ldg(in + Q + i) : -1;
-        const unsigned neg = __ballot_sync(0xffffffffu, valid && e < 0);
-        const unsigned before = neg & lanemask_lt();
-        const int r = before ? (32 - __clz(before)) : 0;  // run start (lane after the last negative)
-        const bool base_pat = (r == 0) ? carry_pat : false;
-        const bool is_pat = valid && e >= 0 && (base_pat ^ (((lane - r) & 1) != 0));
-        const bool is_idx = valid && e >= 0 && !is_pat;
-        int nxt = __shfl_down_sync(0xffffffffu, e, 1);
-        if (lane == 31 && is_idx) nxt = __ldg(in + Q + i + 1);  // pattern sits in the next chunk
-        const int cnt = !valid ? 0 : (e < 0 ? 1 : (is_idx ? __popc(nxt & 0xF) : 0));
-        int tot;
-        const int ex = warp_exclusive_scan(cnt, &tot);
-        const long long o = Z + dpos + ex;
-        if (valid && e < 0) {
-            out[o] = -e;
-        } else if (is_idx) {
-            const unsigned p = (unsigned)nxt & 0xFu;
-            const int b0 = __ffs(p) - 1;
-            int u = 0;
+        int eb[B];
 #pragma unroll
-            for (int b = 0; b < 4; b++)
-                if ((p >> b) & 1u) out[o + u++] = e + S * (b - b0);
+        for (int b = 0; b < B; b++) {
+            const int i = q + 32 * b + lane;
+            eb[b] = (i < nin) ? __ldg(in + Q + i) : -1;
         }
-        const bool last_is_idx = __shfl_sync(0xffffffffu, is_idx, 31);
-        carry_pat = last_is_idx;
-        dpos += tot;
-        q += 32;
+        const int tail = (q + 32 * B < nin) ? __ldg(in + Q + q + 32 * B) : -1;   // first entry after the batch
+#pragma unroll
+        for (int b = 0; b < B; b++) {
+            const int i = q + 32 * b + lane;
+            const bool valid = i < nin;
+            const int e = eb[b];
+            const unsigned neg = __ballot_sync(0xffffffffu, valid && e < 0);
+            const unsigned before = neg & lanemask_lt();
+            const int r = before ? (32 - __clz(before)) : 0;  // run start (lane after the last negative)
+            const bool base_pat = (r == 0) ? carry_pat : false;
+            const bool is_pat = valid && e >= 0 && (base_pat ^ (((lane - r) & 1) != 0));
+            const bool is_idx = valid && e >= 0 && !is_pat;
+            int nxt = __shfl_down_sync(0xffffffffu, e, 1);
+            // lane 31's successor is lane 0 of the next chunk (or the entry after the batch)
+            const int first_next = __shfl_sync(0xffffffffu, (b + 1 < B) ? eb[(b + 1) % B] : tail, 0);
+            if (lane == 31) nxt = (b + 1 < B) ? first_next : tail;
+            const int cnt = !valid ? 0 : (e < 0 ? 1 : (is_idx ? __popc(nxt & 0xF) : 0));
+            int tot;
+            const int ex = warp_exclusive_scan(cnt, &tot);
+            const long long o = Z + dpos + ex;
+            if (valid && e < 0) {
+                out[o] = -e;
+            } else if (is_idx) {
+                const unsigned p = (unsigned)nxt & 0xFu;
+                const int b0 = __ffs(p) - 1;
+                int u = 0;
+#pragma unroll
+                for (int bb = 0; bb < 4; bb++)
+                    if ((p >> bb) & 1u) out[o + u++] = e + S * (bb - b0);
+            }
+            carry_pat = __shfl_sync(0xffffffffu, is_idx, 31);
+            dpos += tot;
+        }
+        q += 32 * B;
     }
 }
 
