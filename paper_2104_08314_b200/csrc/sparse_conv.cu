@@ -339,7 +339,8 @@ struct ConvArgs {
 
 // Strip-kernel configuration: a CTA owns a column strip of TX output columns and
 // all output rows (rt row tiles of TY rows, one per warp), KPL output channels
-// per lane (pairs (k, k+32) as float2 for FFMA2 when KPL is even), CH input
+// per lane (lane owns kbase + lane*KPL + [0, KPL), adjacent pairs as float2 for
+// FFMA2 when KPL is even, so its taps load as one 64/128-bit word), CH input
 // channels staged per chunk.
 template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8, int CH_ = 16>
 struct StripCfg {
@@ -624,17 +625,29 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
             if (!any) continue;
             using WT = typename std::conditional<T::PACKED, float2, float>::type;
+            // lane owns output channels kbase + lane*KPL + [0, KPL): its taps are contiguous
+            // in s_w (one 64/128-bit load per tap)
             WT w[T::NP][T::R][T::S];
 #pragma unroll
-            for (int p = 0; p < T::NP; p++)
+            for (int l = 0; l < T::R; l++)
 #pragma unroll
-                for (int l = 0; l < T::R; l++)
+                for (int m = 0; m < T::S; m++) {
+                    const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane * T::KPL;
+                    if constexpr (T::PACKED && T::KPL % 4 == 0) {
 #pragma unroll
-                    for (int m = 0; m < T::S; m++) {
-                        const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane;
-                        if constexpr (T::PACKED) w[p][l][m] = make_float2(ws[(2 * p) * 32], ws[(2 * p + 1) * 32]);
-                        else w[p][l][m] = ws[p * 32];
+                        for (int p = 0; p < T::NP; p += 2) {
+                            const float4 q4 = *reinterpret_cast<const float4*>(ws + 2 * p);
+                            w[p][l][m] = make_float2(q4.x, q4.y);
+                            w[p + 1][l][m] = make_float2(q4.z, q4.w);
+                        }
+                    } else if constexpr (T::PACKED) {
+#pragma unroll
+                        for (int p = 0; p < T::NP; p++) w[p][l][m] = *reinterpret_cast<const float2*>(ws + 2 * p);
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < T::NP; p++) w[p][l][m] = ws[p];
                     }
+                }
             // hierarchical walk: a warp-uniform branch skips each empty group of 4
             // consecutive window positions, then one per set position
             const float4* w4 = reinterpret_cast<const float4*>(win);
@@ -709,7 +722,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         auto emit = [&](bool add) {
 #pragma unroll
             for (int i = 0; i < T::NACC / 4; i++) {
-                const int k = kbase + (i / NCH) * 32 + lane, oy = rtile * T::TY + (i % NCH);
+                const int k = kbase + lane * T::KPL + (i / NCH), oy = rtile * T::TY + (i % NCH);
                 if (k >= g.K || oy >= g.Oh) continue;
                 float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
                 if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
@@ -767,8 +780,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 #pragma unroll
             for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
             if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
-            const int c = ci / rows, row = ci % rows;
-            const int k = kbase + (row & (T::KB - 1)), oy = (row / T::KB) * T::TY + c;
+            const int c = ci / rows, row = ci % rows, kl = row & (T::KB - 1);   // kl = j*32 + lane
+            const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = (row / T::KB) * T::TY + c;
             if (k >= g.K || oy >= g.Oh) continue;
             float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
             if (vec_ok && ox0 + 3 < g.Ow) {
@@ -814,8 +827,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 #pragma unroll
         for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
         if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
-        const int kl = row & (T::KB - 1), rr = row / T::KB;
-        const int k = kbase + kl, oy = rr * T::TY + c;   // chunk c = output row c of the tile
+        const int kl = row & (T::KB - 1), rr = row / T::KB;   // kl = j*32 + lane
+        const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = rr * T::TY + c;   // chunk c = output row c
         if (k >= g.K || oy >= g.Oh) continue;
         float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
         if (vec_ok && ox0 + 3 < g.Ow) {
