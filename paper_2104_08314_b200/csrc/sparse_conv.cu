@@ -23,6 +23,7 @@
 //    accumulators and runtime tap loops.
 #include <algorithm>
 #include <type_traits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -333,8 +334,13 @@ struct ConvArgs {
     int pmax;       // longest ptr segment of one channel
     int rt;         // strip kernel: row tiles per strip (warps per channel split)
     int csplit;     // strip kernel: channel splits inside the CTA
-    float* scratch; // strip kernel, cg > 1: per-CTA partials for the L2 cluster reduction (or null)
+    float* scratch; // strip kernel: cg > 1 per-CTA partials of the L2 cluster reduction, or
+                    // the balanced mode's published partials (or null)
     size_t scratch_bytes;
+    unsigned* sk_flags;   // balanced mode: one "partial published" flag per CTA (zeroed after use)
+    int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
+    int sk_strips;        // balanced mode: column strips per image (unit = (k-block, image, strip))
+    long long sk_units;   // balanced mode: strips x images x k-blocks
 };
 
 // Strip-kernel configuration: a CTA owns a column strip of TX output columns and
@@ -460,6 +466,40 @@ __device__ __forceinline__ void tap_fma1(int P, float v, float (&acc)[T::NP][T::
         }
 }
 
+// Balanced mode: work of one input channel of a unit in column strip sx, in column
+// equivalents: a fixed part (tap staging, directory) plus the input columns of the
+// strip's window that lie inside the map (the NZEs it scatters and walks).
+constexpr int kSkBaseWork = 15;   // fitted: a chunk of the 3-column edge strip costs 0.86x (cfg5-L8)
+template <class T>
+__device__ __forceinline__ int sk_strip_work(const Geom& g, int sx) {
+    const int w0 = sx * T::TX * T::SW;
+    const int lo = max(w0, g.pl), hi = min(w0 + T::WW, g.pl + g.W);
+    return kSkBaseWork + max(0, hi - lo);
+}
+
+// First work index (unit * C + channel, units ordered k-block, image, strip) of
+// balanced-mode CTA b: where the cumulative work reaches b / sk_ctas of the total.
+template <class T>
+__device__ int sk_start(const ConvArgs& a, int b) {
+    const Geom& g = a.g;
+    const long long groups = a.sk_units / a.sk_strips;      // (k-block, image) pairs
+    if (b >= a.sk_ctas) return (int)(a.sk_units * g.C);
+    long long wsum = 0;
+    for (int sx = 0; sx < a.sk_strips; sx++) wsum += sk_strip_work<T>(g, sx);
+    const long long per_group = wsum * g.C;
+    const long long X = (long long)b * (groups * per_group) / a.sk_ctas;
+    const long long grp = X / per_group;
+    long long rem = X - grp * per_group;
+    int sx = 0;
+    for (; sx < a.sk_strips - 1; sx++) {
+        const long long ws = (long long)sk_strip_work<T>(g, sx) * g.C;
+        if (rem < ws) break;
+        rem -= ws;
+    }
+    const int c = (int)min((long long)g.C - 1, rem / sk_strip_work<T>(g, sx));
+    return (int)((grp * a.sk_strips + sx) * g.C + c);
+}
+
 // Strip kernel.  CTA = (image n, column strip of TX outputs, KB output
 // channels, input-channel range of its cluster rank); warp (r, cs) owns row
 // tile r of the strip for the channels cs, cs+csplit, ...  Per chunk of CH
@@ -476,7 +516,7 @@ __device__ __forceinline__ void tap_fma1(int P, float v, float (&acc)[T::NP][T::
 //      cost multiply-adds (Alg. 2 convSpMv), with no indirect branches.
 // Epilogue: reduce the csplit warps of a row tile through smem, then the cg
 // CTAs of the cluster through distributed shared memory; ReLU; NKHW store.
-template <class T>
+template <class T, bool BAL>
 __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
@@ -484,12 +524,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     const int RT = a.rt, CS = a.csplit;
     const int rtile = warp % RT, cs = warp / RT;
-    const int n = blockIdx.z / a.cg;
     const int rank = (a.cg > 1) ? (int)cgrp::this_cluster().block_rank() : 0;
-    const int kbase = blockIdx.y * T::KB;
-    const int ox0 = blockIdx.x * T::TX, wx0 = ox0 * T::SW;
-    const int cper = (g.C + a.cg - 1) / a.cg;
-    const int c_begin = rank * cper, c_end = min(g.C, c_begin + cper);
+    // current segment: image n, column strip at ox0, k-block at kbase, channels [c_begin, c_end)
+    int n = 0, kbase = 0, ox0 = 0, wx0 = 0, c_begin = 0, c_end = 0;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
@@ -502,20 +539,44 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
 
     using AccT = typename std::conditional<T::PACKED, float2, float>::type;
     AccT acc[T::NP][T::TY][T::TX];
-#pragma unroll
-    for (int p = 0; p < T::NP; p++)
-#pragma unroll
-        for (int yy = 0; yy < T::TY; yy++)
-#pragma unroll
-            for (int xx = 0; xx < T::TX; xx++) {
-                if constexpr (T::PACKED) acc[p][yy][xx] = make_float2(0.f, 0.f);
-                else acc[p][yy][xx] = 0.f;
-            }
     const bool w16 = (g.K % 4) == 0;
 
     // channels per chunk (P1: warps stride the channels); a chunk slightly larger than the
     // warp count would leave one warp doing two channels' scatter, so trim it then
     const int CHS = (T::CH % nwarps == 0 || T::CH >= 2 * nwarps) ? T::CH : min(T::CH, nwarps);
+    // Work.  Default grid: one segment per CTA (blockIdx = strip, k-block, image x cluster
+    // rank).  Balanced mode (BAL, a.sk_ctas CTAs, one per resident slot): the units (strip,
+    // k-block, image) x Q chunks of CHS channels are cut into equal contiguous ranges, one
+    // per CTA; a unit split between CTAs is summed by the CTA holding its first chunk
+    // (its last segment) from the partials the others published (their first segment).
+    int t = 0, t1 = 0;   // balanced mode: this CTA's work range, unit * C + channel
+    if constexpr (BAL) {
+        t = sk_start<T>(a, blockIdx.x);
+        t1 = sk_start<T>(a, blockIdx.x + 1);
+    }
+    auto next_segment = [&](bool first) -> bool {
+        if constexpr (BAL) {
+            if (t >= t1) return false;
+            const int u = t / g.C;
+            c_begin = t - u * g.C;
+            c_end = min(g.C, c_begin + (t1 - t));
+            t += c_end - c_begin;
+            const int sx = u % a.sk_strips, r2 = u / a.sk_strips;
+            n = r2 % g.N;
+            kbase = (r2 / g.N) * T::KB;
+            ox0 = sx * T::TX;
+        } else {
+            if (!first) return false;
+            n = blockIdx.z / a.cg;
+            kbase = blockIdx.y * T::KB;
+            ox0 = blockIdx.x * T::TX;
+            const int cper = (g.C + a.cg - 1) / a.cg;
+            c_begin = rank * cper;
+            c_end = min(g.C, c_begin + cper);
+        }
+        wx0 = ox0 * T::SW;
+        return true;
+    };
     // taps W[c][l][m][kbase..+KB) of a chunk -> s_w (cp.async); independent of the encoding
     auto stage_w = [&](int c0, int chn) {
         const float* wsrc = a.wp + (long long)c0 * T::RS * g.K + kbase;   // row (j*RS+rs) at stride K
@@ -534,254 +595,371 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
     };
-    // PDL prologue: the first chunk's taps load while the encoder finishes
-    probe(0);
-    if (c_begin < c_end) stage_w(c_begin, min(CHS, c_end - c_begin));
-    probe(1);
-    pdl_wait();
-    probe(2);
-    for (int c0 = c_begin; c0 < c_end; c0 += CHS) {
-        const int chn = min(CHS, c_end - c0);
-        const long long nc0 = (long long)n * g.C + c0;
-        // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight); zero the windows
-        {
-            const long long pbase = __ldg(a.cpo_off + nc0);
-            const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
-            const int32_t* src = a.ptr + pbase;
-            for (int i = threadIdx.x; i < plen; i += nthreads) cp_async4(s_ptr + i, src + i, 4);
-            if (threadIdx.x < chn) {
-                s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
-                s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
-            }
-            if (c0 != c_begin) stage_w(c0, chn);
-            float4* v4 = reinterpret_cast<float4*>(s_val);
-            for (int i = threadIdx.x; i < chn * RT * T::NCP / 4; i += nthreads) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            cp_async_wait_all();
+    // per segment
+    for (bool first = true; next_segment(first); first = false) {
+#pragma unroll
+        for (int p = 0; p < T::NP; p++)
+#pragma unroll
+            for (int yy = 0; yy < T::TY; yy++)
+#pragma unroll
+                for (int xx = 0; xx < T::TX; xx++) {
+                    if constexpr (T::PACKED) acc[p][yy][xx] = make_float2(0.f, 0.f);
+                    else acc[p][yy][xx] = 0.f;
+                }
+        if (first) {
+            // PDL prologue: the first chunk's taps load while the encoder finishes
+            probe(0);
+            if (c_begin < c_end) stage_w(c_begin, min(CHS, c_end - c_begin));
+            probe(1);
+            pdl_wait();
+            probe(2);
         }
-        __syncthreads();
-        if (c0 == c_begin) probe(3);
-        // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
-        for (int j = warp; j < chn; j += nwarps) {
-            const int* seg = s_ptr + s_poff[j];
-            DirS<T::S> d;
-            parse_dir<T::S>(g, seg, d);
-            if (d.npc) continue;                                  // NPC: skip channel
-            int lo = 0, hi = 0;
-            if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
-            int tot;
-            const int pre = warp_exclusive_scan(hi - lo, &tot);
-            int* spre = s_scr + warp * 64;
-            int* slo = spre + 32;
-            spre[lane] = (lane < T::WW) ? pre : (1 << 30);
-            slo[lane] = lo;
-            const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
-            const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
-            __syncwarp();
-            const long long Z = s_z[j];
-            float* win = s_val + j * RT * T::NCP;
-            constexpr int U = 4;
-            for (int f0 = 0; f0 < tot; f0 += 32 * U) {
-                int e[U], col[U];
-                float v[U];
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const int f = f0 + 32 * u + lane;
-                    e[u] = -1;
-                    v[u] = 0.f;
-                    col[u] = 0;
-                    if (f < tot) {
-                        int jc = 0;
-#pragma unroll
-                        for (int step = 16; step > 0; step >>= 1)
-                            if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
-                        col[u] = jc;
-                        const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
-                        e[u] = __ldg(a.in + Z + idx);
-                        v[u] = __ldg(a.da + Z + idx);
-                    }
+        for (int c0 = c_begin; c0 < c_end; c0 += CHS) {
+            const int chn = min(CHS, c_end - c0);
+            const long long nc0 = (long long)n * g.C + c0;
+            // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight); zero the windows
+            {
+                const long long pbase = __ldg(a.cpo_off + nc0);
+                const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
+                const int32_t* src = a.ptr + pbase;
+                for (int i = threadIdx.x; i < plen; i += nthreads) cp_async4(s_ptr + i, src + i, 4);
+                if (threadIdx.x < chn) {
+                    s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
+                    s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
                 }
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    if (e[u] < 0) continue;
-                    const int h = e[u] / T::S;                 // IN = L + h*S with L < S
-                    // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
-                    const int rhi = min(RT - 1, h / T::RSTEP);
-                    const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
-                    for (int r = rlo; r <= rhi; r++) win[r * T::NCP + (h - r * T::RSTEP) * T::WW + col[u]] = v[u];
-                }
+                if (!first || c0 != c_begin) stage_w(c0, chn);
+                float4* v4 = reinterpret_cast<float4*>(s_val);
+                for (int i = threadIdx.x; i < chn * RT * T::NCP / 4; i += nthreads) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                cp_async_wait_all();
             }
-        }
-        __syncthreads();
-        if (c0 == c_begin) probe(4);
-        // ---- P2: unrolled walk over the window positions of this warp's row tile
-        for (int j = cs; j < chn; j += CS) {
-            const float* win = s_val + (j * RT + rtile) * T::NCP;
-            unsigned mw[T::MW];
-            bool any = false;
+            __syncthreads();
+            if (c0 == c_begin) probe(3);
+            // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
+            for (int j = warp; j < chn; j += nwarps) {
+                const int* seg = s_ptr + s_poff[j];
+                DirS<T::S> d;
+                parse_dir<T::S>(g, seg, d);
+                if (d.npc) continue;                                  // NPC: skip channel
+                int lo = 0, hi = 0;
+                if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                int tot;
+                const int pre = warp_exclusive_scan(hi - lo, &tot);
+                int* spre = s_scr + warp * 64;
+                int* slo = spre + 32;
+                spre[lane] = (lane < T::WW) ? pre : (1 << 30);
+                slo[lane] = lo;
+                const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
+                const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
+                __syncwarp();
+                const long long Z = s_z[j];
+                float* win = s_val + j * RT * T::NCP;
+                constexpr int U = 4;
+                for (int f0 = 0; f0 < tot; f0 += 32 * U) {
+                    int e[U], col[U];
+                    float v[U];
 #pragma unroll
-            for (int q = 0; q < T::MW; q++) {
-                mw[q] = __ballot_sync(0xffffffffu, win[32 * q + lane] != 0.0f);
-                any |= mw[q] != 0;
-            }
-            if (!any) continue;
-            using WT = typename std::conditional<T::PACKED, float2, float>::type;
-            // lane owns output channels kbase + lane*KPL + [0, KPL): its taps are contiguous
-            // in s_w (one 64/128-bit load per tap)
-            WT w[T::NP][T::R][T::S];
+                    for (int u = 0; u < U; u++) {
+                        const int f = f0 + 32 * u + lane;
+                        e[u] = -1;
+                        v[u] = 0.f;
+                        col[u] = 0;
+                        if (f < tot) {
+                            int jc = 0;
 #pragma unroll
-            for (int l = 0; l < T::R; l++)
-#pragma unroll
-                for (int m = 0; m < T::S; m++) {
-                    const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane * T::KPL;
-                    if constexpr (T::PACKED && T::KPL % 4 == 0) {
-#pragma unroll
-                        for (int p = 0; p < T::NP; p += 2) {
-                            const float4 q4 = *reinterpret_cast<const float4*>(ws + 2 * p);
-                            w[p][l][m] = make_float2(q4.x, q4.y);
-                            w[p + 1][l][m] = make_float2(q4.z, q4.w);
-                        }
-                    } else if constexpr (T::PACKED) {
-#pragma unroll
-                        for (int p = 0; p < T::NP; p++) w[p][l][m] = *reinterpret_cast<const float2*>(ws + 2 * p);
-                    } else {
-#pragma unroll
-                        for (int p = 0; p < T::NP; p++) w[p][l][m] = ws[p];
-                    }
-                }
-            // hierarchical walk: a warp-uniform branch skips each empty group of 4
-            // consecutive window positions, then one per set position
-            const float4* w4 = reinterpret_cast<const float4*>(win);
-            constexpr int NQ = (T::NCASE + 3) / 4;
-            float4 vn = lds128(w4);                      // prefetch: issued ahead of each skip branch
-#pragma unroll
-            for (int q = 0; q < NQ; q++) {
-                const unsigned nib = (mw[q >> 3] >> ((q & 7) * 4)) & 0xFu;
-                const float4 v4 = vn;
-                if (q + 1 < NQ) vn = lds128(w4 + q + 1);
-                if (nib) {
-                    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int P = 4 * q + u;
-                        if (P < T::NCASE && ((nib >> u) & 1u)) {
-                            if constexpr (T::PACKED) tap_fma<T>(P, vv[u], acc, w);
-                            else tap_fma1<T>(P, vv[u], acc, w);
+                            for (int step = 16; step > 0; step >>= 1)
+                                if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                            col[u] = jc;
+                            const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
+                            e[u] = __ldg(a.in + Z + idx);
+                            v[u] = __ldg(a.da + Z + idx);
                         }
                     }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        if (e[u] < 0) continue;
+                        const int h = e[u] / T::S;                 // IN = L + h*S with L < S
+                        // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
+                        const int rhi = min(RT - 1, h / T::RSTEP);
+                        const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
+                        for (int r = rlo; r <= rhi; r++) win[r * T::NCP + (h - r * T::RSTEP) * T::WW + col[u]] = v[u];
+                    }
                 }
             }
+            __syncthreads();
+            if (c0 == c_begin) probe(4);
+            // ---- P2: unrolled walk over the window positions of this warp's row tile
+            for (int j = cs; j < chn; j += CS) {
+                const float* win = s_val + (j * RT + rtile) * T::NCP;
+                unsigned mw[T::MW];
+                bool any = false;
+#pragma unroll
+                for (int q = 0; q < T::MW; q++) {
+                    mw[q] = __ballot_sync(0xffffffffu, win[32 * q + lane] != 0.0f);
+                    any |= mw[q] != 0;
+                }
+                if (!any) continue;
+                using WT = typename std::conditional<T::PACKED, float2, float>::type;
+                // lane owns output channels kbase + lane*KPL + [0, KPL): its taps are contiguous
+                // in s_w (one 64/128-bit load per tap)
+                WT w[T::NP][T::R][T::S];
+#pragma unroll
+                for (int l = 0; l < T::R; l++)
+#pragma unroll
+                    for (int m = 0; m < T::S; m++) {
+                        const float* ws = s_w + (j * T::RS + l * T::S + m) * T::KB + lane * T::KPL;
+                        if constexpr (T::PACKED && T::KPL % 4 == 0) {
+#pragma unroll
+                            for (int p = 0; p < T::NP; p += 2) {
+                                const float4 q4 = *reinterpret_cast<const float4*>(ws + 2 * p);
+                                w[p][l][m] = make_float2(q4.x, q4.y);
+                                w[p + 1][l][m] = make_float2(q4.z, q4.w);
+                            }
+                        } else if constexpr (T::PACKED) {
+#pragma unroll
+                            for (int p = 0; p < T::NP; p++) w[p][l][m] = *reinterpret_cast<const float2*>(ws + 2 * p);
+                        } else {
+#pragma unroll
+                            for (int p = 0; p < T::NP; p++) w[p][l][m] = ws[p];
+                        }
+                    }
+                // hierarchical walk: a warp-uniform branch skips each empty group of 4
+                // consecutive window positions, then one per set position
+                const float4* w4 = reinterpret_cast<const float4*>(win);
+                constexpr int NQ = (T::NCASE + 3) / 4;
+                float4 vn = lds128(w4);                      // prefetch: issued ahead of each skip branch
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    const unsigned nib = (mw[q >> 3] >> ((q & 7) * 4)) & 0xFu;
+                    const float4 v4 = vn;
+                    if (q + 1 < NQ) vn = lds128(w4 + q + 1);
+                    if (nib) {
+                        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int P = 4 * q + u;
+                            if (P < T::NCASE && ((nib >> u) & 1u)) {
+                                if constexpr (T::PACKED) tap_fma<T>(P, vv[u], acc, w);
+                                else tap_fma1<T>(P, vv[u], acc, w);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
 
-    probe(5);
-    // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
-    //      part = [RT*KB rows][TT positions], 16-byte chunks swizzled by (row & (NCH-1))
-    //      so the lane-per-row float4 stores and the chunk-per-thread reads are conflict-free
-    constexpr int TT = T::TY * T::TX, NCH = TT / 4;
-    static_assert(T::TX == 4 && (TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "tile layout");
-    float accf[T::NACC];   // index kk*TT + t
+        probe(5);
+        // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
+        //      part = [RT*KB rows][TT positions], 16-byte chunks swizzled by (row & (NCH-1))
+        //      so the lane-per-row float4 stores and the chunk-per-thread reads are conflict-free
+        constexpr int TT = T::TY * T::TX, NCH = TT / 4;
+        static_assert(T::TX == 4 && (TT & (TT - 1)) == 0 && (T::KB & (T::KB - 1)) == 0, "tile layout");
+        float accf[T::NACC];   // index kk*TT + t
 #pragma unroll
-    for (int p = 0; p < T::NP; p++)
+        for (int p = 0; p < T::NP; p++)
 #pragma unroll
-        for (int t = 0; t < TT; t++) {
-            if constexpr (T::PACKED) {
-                accf[(2 * p) * TT + t] = acc[p][t / T::TX][t % T::TX].x;
-                accf[(2 * p + 1) * TT + t] = acc[p][t / T::TX][t % T::TX].y;
-            } else {
-                accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
+            for (int t = 0; t < TT; t++) {
+                if constexpr (T::PACKED) {
+                    accf[(2 * p) * TT + t] = acc[p][t / T::TX][t % T::TX].x;
+                    accf[(2 * p + 1) * TT + t] = acc[p][t / T::TX][t % T::TX].y;
+                } else {
+                    accf[p * TT + t] = acc[p][t / T::TX][t % T::TX];
+                }
+            }
+        float4* part4 = reinterpret_cast<float4*>(s_w);   // [RT*KB][NCH]
+        float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
+        const bool vec_ok = (g.Ow % 4) == 0;
+        if (CS > 1) {
+            float4* red4 = part4 + RT * T::KB * NCH;       // [CS-1][RT][NACC/4][32]
+            if (cs > 0) {
+#pragma unroll
+                for (int i = 0; i < T::NACC / 4; i++)
+                    red4[(((cs - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane] =
+                        make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+            }
+            __syncthreads();
+            if (cs == 0) {
+                for (int q = 1; q < CS; q++) {
+#pragma unroll
+                    for (int i = 0; i < T::NACC / 4; i++) {
+                        const float4 v = red4[(((q - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane];
+                        accf[4 * i] += v.x; accf[4 * i + 1] += v.y; accf[4 * i + 2] += v.z; accf[4 * i + 3] += v.w;
+                    }
+                }
             }
         }
-    float4* part4 = reinterpret_cast<float4*>(s_w);   // [RT*KB][NCH]
-    float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
-    const bool vec_ok = (g.Ow % 4) == 0;
-    if (CS > 1) {
-        float4* red4 = part4 + RT * T::KB * NCH;       // [CS-1][RT][NACC/4][32]
-        if (cs > 0) {
-#pragma unroll
-            for (int i = 0; i < T::NACC / 4; i++)
-                red4[(((cs - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane] =
-                    make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
-        }
-        __syncthreads();
-        if (cs == 0) {
-            for (int q = 1; q < CS; q++) {
+        if (a.cg == 1) {
+            // no cluster split: store straight from registers (a lane owns output channel
+            // kk*32+lane and a 4-wide output row per accumulator chunk).  With a cluster split
+            // the DSMEM reduction below wins: measured, red.global.add.v4 of every rank's
+            // partial costs 8x the transactions and is slower at cfg2/cfg3.
+            auto emit = [&](bool add) {
 #pragma unroll
                 for (int i = 0; i < T::NACC / 4; i++) {
-                    const float4 v = red4[(((q - 1) * RT + rtile) * (T::NACC / 4) + i) * 32 + lane];
-                    accf[4 * i] += v.x; accf[4 * i + 1] += v.y; accf[4 * i + 2] += v.z; accf[4 * i + 3] += v.w;
+                    const int k = kbase + lane * T::KPL + (i / NCH), oy = rtile * T::TY + (i % NCH);
+                    if (k >= g.K || oy >= g.Oh) continue;
+                    float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+                    if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+                    float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
+                    if (vec_ok && ox0 + 3 < g.Ow) {
+                        if (add)
+                            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                                         ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+                        else
+                            *reinterpret_cast<float4*>(dst) = v;
+                    } else {
+                        const float sv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            if (ox0 + q < g.Ow) {
+                                if (add) atomicAdd(dst + q, sv[q]);
+                                else dst[q] = sv[q];
+                            }
+                    }
+                }
+            };
+            if (!BAL || (c_begin == 0 && c_end == g.C)) {   // whole unit
+            if (cs == 0) emit(false);
+        } else if constexpr (BAL) {
+            const int rows = RT * T::KB;
+            float4* part = reinterpret_cast<float4*>(a.scratch);     // [sk_ctas][NCH][rows]
+            if (c_begin > 0) {
+                // not the unit's first channel: this is the CTA's first segment; publish it
+                float4* mine = part + (long long)blockIdx.x * rows * NCH;
+                if (cs == 0) {
+#pragma unroll
+                    for (int i = 0; i < T::NACC / 4; i++)
+                        __stcg(mine + (i % NCH) * rows + rtile * T::KB + (i / NCH) * 32 + lane,
+                               make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]));
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    st_release32(a.sk_flags + blockIdx.x, 1u);
+                }
+            } else {
+                // the unit's first channel: the CTA's last segment.  The rest of the unit is the
+                // first segment of the next non-empty CTA(s) whose ranges start before its end.
+                const int uend = t - c_end + g.C;
+                if (threadIdx.x == 0) {
+                    int sb = sk_start<T>(a, blockIdx.x + 1);
+                    for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
+                        const int sn = sk_start<T>(a, b + 1);
+                        if (sn > sb)
+                            while (ld_acquire32(a.sk_flags + b) == 0u) __nanosleep(64);
+                        sb = sn;
+                    }
+                }
+                __syncthreads();
+                if (cs == 0) {
+                    int sb = sk_start<T>(a, blockIdx.x + 1);
+                    for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
+                        const int sn = sk_start<T>(a, b + 1);
+                        if (sn > sb) {
+                            const float4* src = part + (long long)b * rows * NCH;
+#pragma unroll
+                            for (int i = 0; i < T::NACC / 4; i++) {
+                                const float4 v = __ldcg(src + (i % NCH) * rows + rtile * T::KB + (i / NCH) * 32 + lane);
+                                accf[4 * i] += v.x; accf[4 * i + 1] += v.y; accf[4 * i + 2] += v.z; accf[4 * i + 3] += v.w;
+                            }
+                        }
+                        sb = sn;
+                    }
+                    emit(false);
+                }
+                if (threadIdx.x == 0) {   // consumed: leave the flags zeroed for the next launch
+                    int sb = sk_start<T>(a, blockIdx.x + 1);
+                    for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
+                        a.sk_flags[b] = 0u;
+                        sb = sk_start<T>(a, b + 1);
+                    }
                 }
             }
         }
-    }
-    if (a.cg == 1) {
-        // no cluster split: store straight from registers (a lane owns output channel
-        // kk*32+lane and a 4-wide output row per accumulator chunk).  With a cluster split
-        // the DSMEM reduction below wins: measured, red.global.add.v4 of every rank's
-        // partial costs 8x the transactions and is slower at cfg2/cfg3.
-        auto emit = [&](bool add) {
+        __syncthreads();   // the epilogue's smem (aliasing the taps) is reused by the next segment
+            continue;
+        }
+        if (a.scratch) {
+            // cluster split, reduced through L2: each CTA stores its partial ([NCH][RT*KB] float4,
+            // coalesced along rows), one cluster barrier (release / acquire) publishes them, then
+            // each rank sums its share of the chunks over the cg partials (L2 reads, all peers'
+            // loads in flight).  Measured: DSMEM moves this traffic ~10x slower on this part
+            // (tools/microbench/dsmem.cu).
+            const int rows = RT * T::KB;
+            const long long slot0 = ((long long)(blockIdx.z - rank) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            const long long sstride = (long long)gridDim.y * gridDim.x;       // next cluster rank
+            float4* mine = reinterpret_cast<float4*>(a.scratch) + (slot0 + rank * sstride) * (long long)rows * NCH;
+            if (cs == 0) {
 #pragma unroll
-            for (int i = 0; i < T::NACC / 4; i++) {
-                const int k = kbase + lane * T::KPL + (i / NCH), oy = rtile * T::TY + (i % NCH);
-                if (k >= g.K || oy >= g.Oh) continue;
-                float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
-                if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
-                float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
-                if (vec_ok && ox0 + 3 < g.Ow) {
-                    if (add)
-                        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
-                                     ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-                    else
-                        *reinterpret_cast<float4*>(dst) = v;
-                } else {
-                    const float sv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int q = 0; q < 4; q++)
-                        if (ox0 + q < g.Ow) {
-                            if (add) atomicAdd(dst + q, sv[q]);
-                            else dst[q] = sv[q];
-                        }
+                for (int i = 0; i < T::NACC / 4; i++) {
+                    const int row = rtile * T::KB + (i / NCH) * 32 + lane, c = i % NCH;
+                    mine[(long long)c * rows + row] = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
                 }
             }
-        };
-        if (cs == 0) emit(false);
-        probe(8);
-        return;
-    }
-    if (a.scratch) {
-        // cluster split, reduced through L2: each CTA stores its partial ([NCH][RT*KB] float4,
-        // coalesced along rows), one cluster barrier (release / acquire) publishes them, then
-        // each rank sums its share of the chunks over the cg partials (L2 reads, all peers'
-        // loads in flight).  Measured: DSMEM moves this traffic ~10x slower on this part
-        // (tools/microbench/dsmem.cu).
-        const int rows = RT * T::KB;
-        const long long slot0 = ((long long)(blockIdx.z - rank) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-        const long long sstride = (long long)gridDim.y * gridDim.x;       // next cluster rank
-        float4* mine = reinterpret_cast<float4*>(a.scratch) + (slot0 + rank * sstride) * (long long)rows * NCH;
+            probe(6);
+            cgrp::this_cluster().sync();
+            probe(7);
+            const int total = rows * NCH;
+            const int per = (total + a.cg - 1) / a.cg;
+            const float4* base = reinterpret_cast<const float4*>(a.scratch) + slot0 * (long long)rows * NCH;
+            const long long pstride = sstride * (long long)rows * NCH;
+            for (int ci = rank * per + threadIdx.x; ci < min(total, (rank + 1) * per); ci += nthreads) {
+                float4 v[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? __ldcg(base + r * pstride + ci) : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 sum = v[0];
+#pragma unroll
+                for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
+                if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
+                const int c = ci / rows, row = ci % rows, kl = row & (T::KB - 1);   // kl = j*32 + lane
+                const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = (row / T::KB) * T::TY + c;
+                if (k >= g.K || oy >= g.Oh) continue;
+                float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
+                if (vec_ok && ox0 + 3 < g.Ow) {
+                    *reinterpret_cast<float4*>(dst) = sum;
+                } else {
+                    const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (ox0 + q < g.Ow) dst[q] = sv[q];
+                }
+            }
+            probe(9);
+            probe(8);
+            return;
+        }
         if (cs == 0) {
 #pragma unroll
             for (int i = 0; i < T::NACC / 4; i++) {
                 const int row = rtile * T::KB + (i / NCH) * 32 + lane, c = i % NCH;
-                mine[(long long)c * rows + row] = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
+                part4[row * NCH + (c ^ (row & (NCH - 1)))] =
+                    make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
             }
         }
         probe(6);
-        cgrp::this_cluster().sync();
+        if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
         probe(7);
-        const int total = rows * NCH;
+        // ---- sum the cluster's partials (DSMEM, all peers' float4 loads in flight), ReLU,
+        //      NKHW store (a chunk = 4 consecutive output columns of one row)
+        const int total = RT * T::KB * NCH;
         const int per = (total + a.cg - 1) / a.cg;
-        const float4* base = reinterpret_cast<const float4*>(a.scratch) + slot0 * (long long)rows * NCH;
-        const long long pstride = sstride * (long long)rows * NCH;
-        for (int ci = rank * per + threadIdx.x; ci < min(total, (rank + 1) * per); ci += nthreads) {
+        const int i0 = rank * per, i1 = min(total, i0 + per);
+        auto cl = cgrp::this_cluster();
+        const float4* peer[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) peer[r] = (a.cg > 1 && r < a.cg) ? cl.map_shared_rank(part4, r) : part4;
+        for (int ci = i0 + threadIdx.x; ci < i1; ci += nthreads) {
+            const int row = ci / NCH, c = ci % NCH;
+            const int sidx = row * NCH + (c ^ (row & (NCH - 1)));
             float4 v[8];
 #pragma unroll
-            for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? __ldcg(base + r * pstride + ci) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? peer[r][sidx] : make_float4(0.f, 0.f, 0.f, 0.f);
             float4 sum = v[0];
 #pragma unroll
             for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
             if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
-            const int c = ci / rows, row = ci % rows, kl = row & (T::KB - 1);   // kl = j*32 + lane
-            const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = (row / T::KB) * T::TY + c;
+            const int kl = row & (T::KB - 1), rr = row / T::KB;   // kl = j*32 + lane
+            const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = rr * T::TY + c;   // chunk c = output row c
             if (k >= g.K || oy >= g.Oh) continue;
             float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
             if (vec_ok && ox0 + 3 < g.Ow) {
@@ -794,55 +972,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
         probe(9);
+        if (a.cg > 1) cl.sync();
         probe(8);
-        return;
     }
-    if (cs == 0) {
-#pragma unroll
-        for (int i = 0; i < T::NACC / 4; i++) {
-            const int row = rtile * T::KB + (i / NCH) * 32 + lane, c = i % NCH;
-            part4[row * NCH + (c ^ (row & (NCH - 1)))] =
-                make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
-        }
-    }
-    probe(6);
-    if (a.cg > 1) cgrp::this_cluster().sync(); else __syncthreads();
-    probe(7);
-    // ---- sum the cluster's partials (DSMEM, all peers' float4 loads in flight), ReLU,
-    //      NKHW store (a chunk = 4 consecutive output columns of one row)
-    const int total = RT * T::KB * NCH;
-    const int per = (total + a.cg - 1) / a.cg;
-    const int i0 = rank * per, i1 = min(total, i0 + per);
-    auto cl = cgrp::this_cluster();
-    const float4* peer[8];
-#pragma unroll
-    for (int r = 0; r < 8; r++) peer[r] = (a.cg > 1 && r < a.cg) ? cl.map_shared_rank(part4, r) : part4;
-    for (int ci = i0 + threadIdx.x; ci < i1; ci += nthreads) {
-        const int row = ci / NCH, c = ci % NCH;
-        const int sidx = row * NCH + (c ^ (row & (NCH - 1)));
-        float4 v[8];
-#pragma unroll
-        for (int r = 0; r < 8; r++) v[r] = (r < a.cg) ? peer[r][sidx] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 sum = v[0];
-#pragma unroll
-        for (int r = 1; r < 8; r++) { sum.x += v[r].x; sum.y += v[r].y; sum.z += v[r].z; sum.w += v[r].w; }
-        if (a.relu) { sum.x = fmaxf(sum.x, 0.f); sum.y = fmaxf(sum.y, 0.f); sum.z = fmaxf(sum.z, 0.f); sum.w = fmaxf(sum.w, 0.f); }
-        const int kl = row & (T::KB - 1), rr = row / T::KB;   // kl = j*32 + lane
-        const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = rr * T::TY + c;   // chunk c = output row c
-        if (k >= g.K || oy >= g.Oh) continue;
-        float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
-        if (vec_ok && ox0 + 3 < g.Ow) {
-            *reinterpret_cast<float4*>(dst) = sum;
-        } else {
-            const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (ox0 + q < g.Ow) dst[q] = sv[q];
-        }
-    }
-    probe(9);
-    if (a.cg > 1) cl.sync();
-    probe(8);
 }
 
 // Generic variant: any R, S, stride; TY x TX = 4 x 4 tile, accumulators in smem.
@@ -934,8 +1066,30 @@ template <class T>
 struct StripPlan {
     int strips, kblocks, rt, csplit, cg;
     long long ctas;
-    size_t scratch_bytes;   // L2 partials when cg > 1
+    size_t scratch_bytes;   // L2 partials: cluster split (cg > 1) or balanced mode, whichever is larger
+    size_t sk_slot_bytes;   // balanced mode: one CTA's published partial
 };
+
+// Balanced mode: at most kSkMaxCtas persistent CTAs (resident slots), one flag each at
+// the head of the conv scratch region.
+constexpr int kSkMaxCtas = 320;
+constexpr size_t kSkFlagBytes = ((kSkMaxCtas * sizeof(unsigned)) + 255) / 256 * 256;
+
+// Development override: SPC_BALANCE=0 disables the balanced mode.
+static bool balance_enabled() {
+    static const char* env = getenv("SPC_BALANCE");
+    return !env || atoi(env) != 0;
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            n = 148;
+    }
+    return n;
+}
 template <class T>
 static StripPlan<T> plan_strip(const Geom& g) {
     StripPlan<T> p;
@@ -947,30 +1101,22 @@ static StripPlan<T> plan_strip(const Geom& g) {
     int cg = tune_cg();
     if (cg <= 0) cg = pick_cg(p.ctas, g.C, T::MINB);
     p.cg = cg;
-    p.scratch_bytes = (cg > 1) ? (size_t)p.ctas * cg * p.rt * T::KB * (T::TY * T::TX) * sizeof(float) : 0;
+    p.sk_slot_bytes = (size_t)p.rt * T::KB * (T::TY * T::TX) * sizeof(float);
+    p.scratch_bytes = std::max((cg > 1) ? (size_t)p.ctas * cg * p.sk_slot_bytes : 0,
+                               (cg == 1) ? (size_t)kSkMaxCtas * p.sk_slot_bytes : 0);
     return p;
 }
 
-template <class T>
-static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
-    const Geom& g = a.g;
-    const StripPlan<T> pl = plan_strip<T>(g);
-    const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
-    a.rt = pl.rt;
-    if (a.rt > T::MAXW) return cudaErrorInvalidValue;
-    a.csplit = pl.csplit;
-    a.cg = cg;
-    if (cg <= 1 || a.scratch_bytes < pl.scratch_bytes) a.scratch = nullptr;
-    const size_t smem = strip_smem<T>(a);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+template <class T, bool BAL>
+static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t smem, cudaStream_t st) {
     static size_t attr_bytes = 0;     // per instantiation
     if (attr_bytes < smem) {
-        cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T, BAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
         attr_bytes = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(strips, kblocks, g.N * cg);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(32 * a.rt * a.csplit);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -983,7 +1129,49 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T>, a);
+    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL>, a);
+}
+
+template <class T>
+static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
+    const Geom& g = a.g;
+    const StripPlan<T> pl = plan_strip<T>(g);
+    const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
+    a.rt = pl.rt;
+    if (a.rt > T::MAXW) return cudaErrorInvalidValue;
+    a.csplit = pl.csplit;
+    a.cg = cg;
+    const size_t smem = strip_smem<T>(a);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    // Balanced mode when the units outnumber the SMs and the busiest SM would get >= 20%
+    // more units than the average (a CTA's time changes little with a second co-resident
+    // CTA, so the SM holding the most units sets the kernel time): one CTA per resident
+    // slot, equal-work channel ranges.  Measured at batch 32 (cfg5): -10..-13% at skew 1.32
+    // (L0, L3), -5% (L4); at skew 1.16 between -5% (L7) and +4% (L12), hence the threshold.
+    a.sk_ctas = 0;
+    a.sk_strips = strips;
+    a.sk_units = pl.ctas;
+    const int nsm = sm_count();
+    const double skew = (double)((pl.ctas + nsm - 1) / nsm) * nsm / (double)pl.ctas;
+    if (cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
+        static int occ = -1;   // per instantiation (same block size and smem for a given T)
+        if (occ < 0) {
+            cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (err != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) !=
+                    cudaSuccess)
+                occ = 0;
+        }
+        const long long P = (long long)occ * nsm;
+        if (P > 0 && P <= kSkMaxCtas && pl.ctas * g.C < (1LL << 31) && a.scratch_bytes >= (size_t)P * pl.sk_slot_bytes)
+            a.sk_ctas = (int)P;
+    }
+    if (!a.sk_ctas && (cg <= 1 || a.scratch_bytes < pl.scratch_bytes)) a.scratch = nullptr;
+    if (getenv("SPC_PLAN_DEBUG"))
+        fprintf(stderr, "strip plan: units %lld strips %d kblocks %d rt %d csplit %d cg %d sk_ctas %d smem %zu\n",
+                pl.ctas, strips, kblocks, a.rt, a.csplit, cg, a.sk_ctas, smem);
+    if (a.sk_ctas) return launch_strip<T, true>(a, dim3(a.sk_ctas, 1, 1), 1, smem, st);
+    return launch_strip<T, false>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
 }
 
 // Calls f(StripCfg<...>{}) for the strip configuration of this geometry; returns
@@ -1013,7 +1201,7 @@ size_t conv_scratch_bytes(const Geom& g) {
         bytes = plan_strip<decltype(cfg)>(g).scratch_bytes;
         return cudaSuccess;
     });
-    return bytes;
+    return bytes ? kSkFlagBytes + bytes : 0;
 }
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
@@ -1033,8 +1221,18 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.cg = 1;
     a.rt = 1;
     a.csplit = 1;
-    a.scratch = scratch;
-    a.scratch_bytes = scratch_bytes;
+    // scratch = [balanced-mode flags][partials]
+    a.sk_flags = nullptr;
+    a.scratch = nullptr;
+    a.scratch_bytes = 0;
+    a.sk_ctas = 0;
+    a.sk_strips = 1;
+    a.sk_units = 0;
+    if (scratch && scratch_bytes > kSkFlagBytes) {
+        a.sk_flags = reinterpret_cast<unsigned*>(scratch);
+        a.scratch = scratch + kSkFlagBytes / sizeof(float);
+        a.scratch_bytes = scratch_bytes - kSkFlagBytes;
+    }
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
     cudaError_t err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;

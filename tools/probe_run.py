@@ -73,3 +73,6 @@ for wl in sys.argv[1:] or ["cfg1", "cfg2"]:
     if (te > 0).any() and (tc > 0).any():
         print(f"   conv first stamp - encoder first stamp: {(tc[tc > 0].min() - te[te > 0].min()) / 1e3:.2f} us;"
               f" encoder last stamp -> conv last stamp: {(tc.max() - te.max()) / 1e3:.2f} us")
+    if os.environ.get("PROBE_DUMP"):
+        np.savez(os.path.join(ROOT, "gpurun_out", f"probe_{wl}.npz"), conv=cv, enc=e,
+                 chan_nz_off=L.enc.chan_nz_off.cpu().numpy(), chan_ptr_off=L.enc.chan_ptr_off.cpu().numpy())
