@@ -150,6 +150,30 @@ def test_encoder_multi_round_tiles(oracle_mod, shape):
     _layer_case(oracle_mod, d, x, w, full=False, samples=2000, seed=5)
 
 
+@pytest.mark.parametrize("shape", [(12, 16, 56, 56, 64), (24, 24, 28, 28, 128)])
+def test_balanced_mode_full(oracle_mod, shape, capfd, monkeypatch):
+    """Grids whose units (strip, k-block, image) outnumber the SMs unevenly run in the
+    balanced mode (persistent CTAs over equal-work channel ranges; a unit split between
+    CTAs is summed from flag-published partials).  Full-output parity, ReLU fusion, and
+    bit-identical repeats (the flags must be left zeroed for the next launch)."""
+    N, C, H, W, K = shape
+    d = layer_desc(N, C, H, W, K, 3, 3, 1, 1, 1, 1, 1, 1)
+    x = clustered_relu(N, C, H, W, 0.3, 91, 0.05, 0.1)
+    w = he_normal(K, C, 3, 3, 91)
+    monkeypatch.setenv("SPC_PLAN_DEBUG", "1")
+    L = GpuLayer(d, w)
+    L.encode(torch.from_numpy(x).cuda())
+    assert_streams_equal(L.streams(), oracle_mod.encode(d, x), "balanced")
+    y1 = L.conv().cpu().numpy()
+    err = capfd.readouterr().err
+    assert "sk_ctas 0" not in err and "sk_ctas" in err, err
+    ref = oracle_mod.direct_conv(d, x, w)
+    _check_conv(y1, ref, "balanced mode")
+    for _ in range(3):
+        assert np.array_equal(L.conv().cpu().numpy(), y1)
+    _check_conv(L.conv(relu=True).cpu().numpy(), np.maximum(ref, 0.0), "balanced mode + relu")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _desc3(**kw):
