@@ -319,6 +319,16 @@ cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_
 
 // ------------------------------------------------------------ conv kernels
 
+// Development phase switch (probe build only): 1 = stage/scatter only the first chunk of
+// a segment (times the walk alone), 2 = skip the walk, 3 = stage the taps of the first
+// chunk only, 4 = scatter the first chunk only.  Always 0 in the product library.
+#ifdef SPC_PROBES
+__constant__ int g_dev_phase_mode = 0;
+__device__ __forceinline__ int dev_phase_mode() { return g_dev_phase_mode; }
+#else
+__device__ __forceinline__ constexpr int dev_phase_mode() { return 0; }
+#endif
+
 struct ConvArgs {
     Geom g;
     const int32_t* __restrict__ ptr;
@@ -354,6 +364,7 @@ struct StripCfg {
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
     static constexpr int MAXW = MAXW_, THREADS = 32 * MAXW;
     static constexpr int CH = CH_;        // input channels staged per chunk (fewer chunk barriers when larger)
+    static constexpr int CW = 16 * CH;    // channels whose side-table entries are staged at once
     static constexpr int KB = 32 * KPL;               // output channels per CTA
     static constexpr int RS = R * S;
     static constexpr int NACC = KPL * TY * TX;        // accumulators per lane
@@ -531,11 +542,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* s_w = reinterpret_cast<float*>(smem_raw);                                  // [CH][RS][KB]
     float* s_val = s_w + T::CH * T::RS * T::KB;                                       // [CH][RT][NCP]
-    int* s_ptr = reinterpret_cast<int*>(s_val + T::CH * RT * T::NCP);                 // [CH * pmax]
-    int* s_poff = s_ptr + T::CH * a.pmax;                                             // [CH]
-    int* s_scr = s_poff + T::CH;                                                      // [MAXW][64]
-    long long* s_z = reinterpret_cast<long long*>(
-        (reinterpret_cast<uintptr_t>(s_scr + T::MAXW * 64) + 7) & ~uintptr_t(7));      // [CH]
+    int* s_ptr = reinterpret_cast<int*>(s_val + T::CH * RT * T::NCP);                 // [2][CH * pmax]
+    int* s_coff = s_ptr + 2 * T::CH * a.pmax;       // [CW + 1] window's ptr offsets - cbase
+    int* s_cz = s_coff + T::CW + 1;                 // [CW + 1] window's DA offsets - zbase
+    int* s_scr = s_cz + T::CW + 1;                  // [MAXW][64]
 
     using AccT = typename std::conditional<T::PACKED, float2, float>::type;
     AccT acc[T::NP][T::TY][T::TX];
@@ -549,18 +559,28 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     // k-block, image) x Q chunks of CHS channels are cut into equal contiguous ranges, one
     // per CTA; a unit split between CTAs is summed by the CTA holding its first chunk
     // (its last segment) from the partials the others published (their first segment).
-    int t = 0, t1 = 0;   // balanced mode: this CTA's work range, unit * C + channel
+    // balanced mode: this CTA's remaining work range [s_seg[0], s_seg[1]) in units of
+    // (unit * C + channel); kept in shared memory (read at segment starts only, so it
+    // does not hold registers through the walk).  s_seg[0] advances after the first
+    // barrier of each segment.
+    __shared__ int s_seg[2];
+    int t_next = 0;
     if constexpr (BAL) {
-        t = sk_start<T>(a, blockIdx.x);
-        t1 = sk_start<T>(a, blockIdx.x + 1);
+        if (threadIdx.x == 0) {
+            s_seg[0] = sk_start<T>(a, blockIdx.x);
+            s_seg[1] = sk_start<T>(a, blockIdx.x + 1);
+        }
+        __syncthreads();
     }
     auto next_segment = [&](bool first) -> bool {
         if constexpr (BAL) {
+            const int t = *reinterpret_cast<volatile int*>(&s_seg[0]);
+            const int t1 = *reinterpret_cast<volatile int*>(&s_seg[1]);
             if (t >= t1) return false;
             const int u = t / g.C;
             c_begin = t - u * g.C;
             c_end = min(g.C, c_begin + (t1 - t));
-            t += c_end - c_begin;
+            t_next = t + c_end - c_begin;
             const int sx = u % a.sk_strips, r2 = u / a.sk_strips;
             n = r2 % g.N;
             kbase = (r2 / g.N) * T::KB;
@@ -595,6 +615,28 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
         }
     };
+    // Side tables of a window of CW channels (one L2 round trip per window instead of one
+    // per chunk) and the ptr segments of the next chunk, prefetched during the walk.
+    int cw0 = 0, cw1 = 0;
+    long long cbase = 0, zbase = 0;
+    auto stage_window = [&](int c) {
+        const long long nc = (long long)n * g.C + c;
+        cw0 = c;
+        cw1 = min(c_end, c + T::CW);
+        cbase = __ldg(a.cpo_off + nc);
+        zbase = __ldg(a.cnz_off + nc);
+        for (int i = threadIdx.x; i <= cw1 - cw0; i += nthreads) {
+            s_coff[i] = (int)(__ldg(a.cpo_off + nc + i) - cbase);
+            s_cz[i] = (int)(__ldg(a.cnz_off + nc + i) - zbase);
+        }
+        __syncthreads();
+    };
+    auto stage_ptr = [&](int c0, int chn, int buf) {
+        const int r0 = s_coff[c0 - cw0], plen = s_coff[c0 - cw0 + chn] - r0;
+        const int32_t* src = a.ptr + cbase + r0;
+        int* dst = s_ptr + buf * T::CH * a.pmax;
+        for (int i = threadIdx.x; i < plen; i += nthreads) cp_async4(dst + i, src + i, 4);
+    };
     // per segment
     for (bool first = true; next_segment(first); first = false) {
 #pragma unroll
@@ -614,29 +656,27 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             pdl_wait();
             probe(2);
         }
-        for (int c0 = c_begin; c0 < c_end; c0 += CHS) {
+        int buf = 0;
+        if (c_begin < c_end) {
+            stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
+            if (BAL && threadIdx.x == 0) s_seg[0] = t_next;
+            stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
+        }
+        for (int c0 = c_begin; c0 < c_end; c0 += CHS, buf ^= 1) {
             const int chn = min(CHS, c_end - c0);
-            const long long nc0 = (long long)n * g.C + c0;
-            // ---- P0: stage ptr segments, DA offsets, taps (cp.async, all in flight); zero the windows
-            {
-                const long long pbase = __ldg(a.cpo_off + nc0);
-                const int plen = (int)(__ldg(a.cpo_off + nc0 + chn) - pbase);
-                const int32_t* src = a.ptr + pbase;
-                for (int i = threadIdx.x; i < plen; i += nthreads) cp_async4(s_ptr + i, src + i, 4);
-                if (threadIdx.x < chn) {
-                    s_poff[threadIdx.x] = (int)(__ldg(a.cpo_off + nc0 + threadIdx.x) - pbase);
-                    s_z[threadIdx.x] = __ldg(a.cnz_off + nc0 + threadIdx.x);
-                }
-                if (!first || c0 != c_begin) stage_w(c0, chn);
+            const bool stage = !(dev_phase_mode() == 1 && !(first && c0 == c_begin));
+            // ---- P0: taps (cp.async, with this chunk's prefetched ptr segments in flight); zero the windows
+            if (stage) {
+                if ((!first || c0 != c_begin) && dev_phase_mode() != 3) stage_w(c0, chn);
                 float4* v4 = reinterpret_cast<float4*>(s_val);
                 for (int i = threadIdx.x; i < chn * RT * T::NCP / 4; i += nthreads) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
                 cp_async_wait_all();
             }
-            __syncthreads();
+            if (stage) __syncthreads();
             if (c0 == c_begin) probe(3);
             // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
-            for (int j = warp; j < chn; j += nwarps) {
-                const int* seg = s_ptr + s_poff[j];
+            for (int j = warp; stage && j < chn && !(dev_phase_mode() == 4 && !(first && c0 == c_begin)); j += nwarps) {
+                const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
                 DirS<T::S> d;
                 parse_dir<T::S>(g, seg, d);
                 if (d.npc) continue;                                  // NPC: skip channel
@@ -651,7 +691,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
                 const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
                 __syncwarp();
-                const long long Z = s_z[j];
+                const long long Z = zbase + s_cz[c0 - cw0 + j];
                 float* win = s_val + j * RT * T::NCP;
                 constexpr int U = 4;
                 for (int f0 = 0; f0 < tot; f0 += 32 * U) {
@@ -685,10 +725,17 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     }
                 }
             }
-            __syncthreads();
+            if (stage) __syncthreads();
             if (c0 == c_begin) probe(4);
+            // prefetch the next chunk's ptr segments (its buffer was last read before the barrier)
+            if (c0 + CHS < c_end && stage) {
+                const int cn = c0 + CHS, chnn = min(CHS, c_end - cn);
+                if (cn + chnn > cw1) stage_window(cn);
+                stage_ptr(cn, chnn, buf ^ 1);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            }
             // ---- P2: unrolled walk over the window positions of this warp's row tile
-            for (int j = cs; j < chn; j += CS) {
+            for (int j = cs; j < chn && dev_phase_mode() != 2; j += CS) {
                 const float* win = s_val + (j * RT + rtile) * T::NCP;
                 unsigned mw[T::MW];
                 bool any = false;
@@ -840,7 +887,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             } else {
                 // the unit's first channel: the CTA's last segment.  The rest of the unit is the
                 // first segment of the next non-empty CTA(s) whose ranges start before its end.
-                const int uend = t - c_end + g.C;
+                const int uend = s_seg[0] - c_end + g.C;   // s_seg[0] = this segment's end
                 if (threadIdx.x == 0) {
                     int sb = sk_start<T>(a, blockIdx.x + 1);
                     for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
@@ -1039,8 +1086,7 @@ template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
-                        (size_t)T::CH * a.pmax * 4 + (size_t)T::CH * 4 + (size_t)T::MAXW * 64 * 4 + 16 +
-                        (size_t)T::CH * 8;
+                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)T::MAXW * 64 * 4;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
@@ -1154,13 +1200,11 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const int nsm = sm_count();
     const double skew = (double)((pl.ctas + nsm - 1) / nsm) * nsm / (double)pl.ctas;
     if (cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
-        static int occ = -1;   // per instantiation (same block size and smem for a given T)
-        if (occ < 0) {
-            cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            if (err != cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) !=
-                    cudaSuccess)
-                occ = 0;
+        int occ = 0;
+        if (cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) != cudaSuccess) {
+            (void)cudaGetLastError();   // not sticky: fall back to the default grid
+            occ = 0;
         }
         const long long P = (long long)occ * nsm;
         if (P > 0 && P <= kSkMaxCtas && pl.ctas * g.C < (1LL << 31) && a.scratch_bytes >= (size_t)P * pl.sk_slot_bytes)
@@ -1262,4 +1306,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
 
 #ifdef SPC_PROBES
 SPC_PROBE_ACCESSOR(spc_debug_probes_conv)
+extern "C" int spc_debug_set_phase_mode(int m) {
+    return (int)cudaMemcpyToSymbol(spc::g_dev_phase_mode, &m, sizeof m);
+}
 #endif

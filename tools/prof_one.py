@@ -6,6 +6,8 @@ from synth import clustered_relu, he_normal
 from paper_2104_08314_b200.layer import SparseConvLayer
 wl = sys.argv[1]
 c = workload(wl); d = c["desc"]
+if len(sys.argv) > 2:
+    d = dict(d, N=int(sys.argv[2]))
 dens = c["density"] if c["density"] is not None else 0.5
 x = clustered_relu(d["N"], d["C"], d["H"], d["W"], dens, c["seed"], c["dead_frac"], c["zero_tile_frac"])
 w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
