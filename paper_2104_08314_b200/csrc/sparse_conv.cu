@@ -358,8 +358,13 @@ struct ConvArgs {
 // per lane (lane owns kbase + lane*KPL + [0, KPL), adjacent pairs as float2 for
 // FFMA2 when KPL is even, so its taps load as one 64/128-bit word), CH input
 // channels staged per chunk.
-template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8, int CH_ = 16>
+template <int R_, int S_, int SH_, int SW_, int TY_, int TX_, int KPL_, int MINB_ = 2, int MAXW_ = 8, int CH_ = 16,
+          bool FLAT_ = false>
 struct StripCfg {
+    // P1 flattened over the chunk's NZEs across channels (one L2 round trip per chunk) instead
+    // of warp per channel: measured faster only where a chunk holds many short channels per
+    // warp AND the walk's code generation is unaffected (set per configuration)
+    static constexpr bool FLAT = FLAT_;
     static constexpr int MINB = MINB_;   // CTAs per SM targeted by the register budget
     static constexpr int R = R_, S = S_, SH = SH_, SW = SW_, TY = TY_, TX = TX_, KPL = KPL_;
     static constexpr int MAXW = MAXW_, THREADS = 32 * MAXW;
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     int* s_ptr = reinterpret_cast<int*>(s_val + T::CH * RT * T::NCP);                 // [2][CH * pmax]
     int* s_coff = s_ptr + 2 * T::CH * a.pmax;       // [CW + 1] window's ptr offsets - cbase
     int* s_cz = s_coff + T::CW + 1;                 // [CW + 1] window's DA offsets - zbase
-    int* s_scr = s_cz + T::CW + 1;                  // [MAXW][64]
+    int* s_scr = s_cz + T::CW + 1;                  // P1 column tables: [CH][65] (FLAT) or [MAXW][64]
 
     using AccT = typename std::conditional<T::PACKED, float2, float>::type;
     AccT acc[T::NP][T::TY][T::TX];
@@ -674,54 +679,124 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
             if (stage) __syncthreads();
             if (c0 == c_begin) probe(3);
-            // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
-            for (int j = warp; stage && j < chn && !(dev_phase_mode() == 4 && !(first && c0 == c_begin)); j += nwarps) {
-                const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
-                DirS<T::S> d;
-                parse_dir<T::S>(g, seg, d);
-                if (d.npc) continue;                                  // NPC: skip channel
-                int lo = 0, hi = 0;
-                if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
-                int tot;
-                const int pre = warp_exclusive_scan(hi - lo, &tot);
-                int* spre = s_scr + warp * 64;
-                int* slo = spre + 32;
-                spre[lane] = (lane < T::WW) ? pre : (1 << 30);
-                slo[lane] = lo;
-                const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
-                const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
-                __syncwarp();
-                const long long Z = zbase + s_cz[c0 - cw0 + j];
-                float* win = s_val + j * RT * T::NCP;
-                constexpr int U = 4;
-                for (int f0 = 0; f0 < tot; f0 += 32 * U) {
-                    int e[U], col[U];
-                    float v[U];
-#pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        const int f = f0 + 32 * u + lane;
-                        e[u] = -1;
-                        v[u] = 0.f;
-                        col[u] = 0;
-                        if (f < tot) {
-                            int jc = 0;
-#pragma unroll
-                            for (int step = 16; step > 0; step >>= 1)
-                                if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
-                            col[u] = jc;
-                            const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
-                            e[u] = __ldg(a.in + Z + idx);
-                            v[u] = __ldg(a.da + Z + idx);
+            if constexpr (T::FLAT) {
+                // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows.
+                //      (a) warp per channel: block directory (NPC / NPF skip) and the DA range of each
+                //      window column -> per-channel column prefix table; (b) all threads over the
+                //      chunk's NZEs flattened across channels, so one L2 round trip covers the chunk.
+                const bool scatter = stage && !(dev_phase_mode() == 4 && !(first && c0 == c_begin));
+                int* fpre = s_scr;                      // [CH][32] column prefix within the channel
+                int* flo = fpre + T::CH * 32;           // [CH][32] DA offset of the column
+                int* ftot = flo + T::CH * 32;           // [CH] NZEs of the channel in the window
+                for (int j = warp; scatter && j < chn; j += nwarps) {
+                    const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
+                    DirS<T::S> d;
+                    parse_dir<T::S>(g, seg, d);
+                    int lo = 0, hi = 0;
+                    if (!d.npc && lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);   // NPC: skip
+                    int tot;
+                    const int pre = warp_exclusive_scan(hi - lo, &tot);
+                    fpre[j * 32 + lane] = (lane < T::WW) ? pre : (1 << 30);
+                    flo[j * 32 + lane] = lo;
+                    if (lane == 0) ftot[j] = tot;
+                }
+                if (scatter) __syncthreads();
+                if (scatter) {
+                    int total;
+                    const int cpre = warp_exclusive_scan(lane < chn ? ftot[lane] : 0, &total);
+                    constexpr int U = 4;
+                    for (int f0 = warp * 32 * U; f0 < total; f0 += nwarps * 32 * U) {
+                        int e[U], pos[U];
+                        float v[U];
+    #pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            const int f = f0 + 32 * u + lane;
+                            // channel: last j with cpre[j] <= f (all lanes shuffle)
+                            int j = 0;
+    #pragma unroll
+                            for (int step = 16; step > 0; step >>= 1) {
+                                const int cand = j + step;
+                                const int cv = __shfl_sync(0xffffffffu, cpre, cand & 31);
+                                if (cand < chn && cv <= f) j = cand;
+                            }
+                            const int fj = f - __shfl_sync(0xffffffffu, cpre, j);
+                            e[u] = -1;
+                            v[u] = 0.f;
+                            pos[u] = 0;
+                            if (f < total) {
+                                const int* jp = fpre + j * 32;
+                                int jc = 0;
+    #pragma unroll
+                                for (int step = 16; step > 0; step >>= 1)
+                                    if (jc + step < T::WW && jp[jc + step] <= fj) jc += step;
+                                const long long Z = zbase + s_cz[c0 - cw0 + j];
+                                const int idx = flo[j * 32 + jc] + (fj - jp[jc]);
+                                e[u] = __ldg(a.in + Z + idx);
+                                v[u] = __ldg(a.da + Z + idx);
+                                pos[u] = j * RT * T::NCP + jc;
+                            }
+                        }
+    #pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            if (e[u] < 0) continue;
+                            const int h = e[u] / T::S;                 // IN = L + h*S with L < S
+                            // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
+                            const int rhi = min(RT - 1, h / T::RSTEP);
+                            const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
+                            for (int r = rlo; r <= rhi; r++) s_val[pos[u] + r * T::NCP + (h - r * T::RSTEP) * T::WW] = v[u];
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        if (e[u] < 0) continue;
-                        const int h = e[u] / T::S;                 // IN = L + h*S with L < S
-                        // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
-                        const int rhi = min(RT - 1, h / T::RSTEP);
-                        const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
-                        for (int r = rlo; r <= rhi; r++) win[r * T::NCP + (h - r * T::RSTEP) * T::WW + col[u]] = v[u];
+                }
+            } else {
+                // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows
+                for (int j = warp; stage && j < chn && !(dev_phase_mode() == 4 && !(first && c0 == c_begin)); j += nwarps) {
+                    const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
+                    DirS<T::S> d;
+                    parse_dir<T::S>(g, seg, d);
+                    if (d.npc) continue;                                  // NPC: skip channel
+                    int lo = 0, hi = 0;
+                    if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                    int tot;
+                    const int pre = warp_exclusive_scan(hi - lo, &tot);
+                    int* spre = s_scr + warp * 64;
+                    int* slo = spre + 32;
+                    spre[lane] = (lane < T::WW) ? pre : (1 << 30);
+                    slo[lane] = lo;
+                    const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
+                    const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
+                    __syncwarp();
+                    const long long Z = zbase + s_cz[c0 - cw0 + j];
+                    float* win = s_val + j * RT * T::NCP;
+                    constexpr int U = 4;
+                    for (int f0 = 0; f0 < tot; f0 += 32 * U) {
+                        int e[U], col[U];
+                        float v[U];
+    #pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            const int f = f0 + 32 * u + lane;
+                            e[u] = -1;
+                            v[u] = 0.f;
+                            col[u] = 0;
+                            if (f < tot) {
+                                int jc = 0;
+    #pragma unroll
+                                for (int step = 16; step > 0; step >>= 1)
+                                    if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                                col[u] = jc;
+                                const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
+                                e[u] = __ldg(a.in + Z + idx);
+                                v[u] = __ldg(a.da + Z + idx);
+                            }
+                        }
+    #pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            if (e[u] < 0) continue;
+                            const int h = e[u] / T::S;                 // IN = L + h*S with L < S
+                            // row tiles whose window [r*RSTEP, r*RSTEP + WH) holds row h (at most 2)
+                            const int rhi = min(RT - 1, h / T::RSTEP);
+                            const int rlo = (h >= T::WH - 1) ? (h - T::WH + 1 + T::RSTEP - 1) / T::RSTEP : 0;
+                            for (int r = rlo; r <= rhi; r++) win[r * T::NCP + (h - r * T::RSTEP) * T::WW + col[u]] = v[u];
+                        }
                     }
                 }
             }
@@ -1086,7 +1161,7 @@ template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
-                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)T::MAXW * 64 * 4;
+                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 65 : T::MAXW * 64) * 4;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
@@ -1224,7 +1299,7 @@ template <class F>
 static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
         if (g.K <= 32 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16, 32>{});
-        if (g.K <= 64 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32>{});
+        if (g.K <= 64 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32, true>{});
         if (g.Oh <= 32) return f(StripCfg<3, 3, 1, 1, 4, 4, 4>{});
         if (g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 4, 1>{});
     } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
@@ -1232,9 +1307,9 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
         if (g.Oh <= 16) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>{});
         if (g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>{});   // 8: keeps 2 CTAs/SM
     } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
-        return f(StripCfg<1, 7, 1, 1, 8, 4, 2>{});
+        return f(StripCfg<1, 7, 1, 1, 8, 4, 2, 2, 8, 16, true>{});
     } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
-        return f(StripCfg<7, 1, 1, 1, 8, 4, 2>{});
+        return f(StripCfg<7, 1, 1, 1, 8, 4, 2, 2, 8, 16, true>{});
     }
     return cudaErrorNotSupported;
 }
