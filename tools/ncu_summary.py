@@ -47,7 +47,9 @@ def launches(path: str):
 def report(path: str, label: str = ""):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
+    unit_of = dict(zip(hdr, units))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
     name_i = hdr.index("Kernel Name")
     print(f"# ncu --set full summary {label}".rstrip())
     for r in rows[2:]:
@@ -55,7 +57,11 @@ def report(path: str, label: str = ""):
         print(f"\n## {vals[hdr[name_i]][:110]}")
         for k, short in KEYS:
             if k in vals:
-                print(f"  {short:22s} {vals[k]}")
+                v = vals[k]
+                u = unit_of.get(k, "")
+                if u in scale and v:   # bytes in bytes, durations in us
+                    v = f"{float(v.replace(',', '')) * scale[u]:.6g}"
+                print(f"  {short:22s} {v}")
         stalls = sorted(((h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
                           float(v.replace(",", "") or 0)) for h, v in vals.items()
                          if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("per_issue_active.ratio")),
