@@ -486,6 +486,41 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
                         }
                     }
                 }
+            } else if (NW <= 2 && (g.W & 7) == 4) {
+                // W = 4 x odd (28, 12, 20, ...): lanes = 4 column items x 8 rows, so the plane
+                // reads hit 32 distinct banks instead of 8 (4-way with lanes = 32 rows of one
+                // column); each lane ranks its NZE in its own column (popc below its row) and the
+                // stores form 4 short runs.  Measured: cfg5-L7 82 -> 71 us, batch-256 L4 203 ->
+                // 176 us; at W = 56 (2-way here vs 8-way) it was slower (34 -> 37 us), so W = 8k
+                // keeps the row-lane pass below.
+                const int cu = lane >> 3, hr = lane & 7;
+                for (int it0 = 4 * warp; it0 < nit; it0 += 4 * kEncWarps) {
+                    const int it = it0 + cu;
+                    const bool v = it < nit;
+                    const int4 t = v ? tab[it] : make_int4(0, 0, 0, 0);
+                    const unsigned m0 = v ? msk[it * NW] : 0u;
+                    const unsigned m1 = (v && NW == 2) ? msk[it * NW + 1] : 0u;
+                    if (!__any_sync(0xffffffffu, (t.w & kTabOk) != 0)) continue;
+                    const bool ok = (t.w & kTabOk) != 0;
+                    const int c0 = __popc(m0);
+                    const int Lc = t.w & 0xFFFF;
+                    const bool win = (t.w & kTabIn) != 0;
+#pragma unroll
+                    for (int rb = 0; rb < 64; rb += 8) {
+                        const int h = rb + hr;                 // padded row
+                        if (rb >= g.Hp) break;
+                        const unsigned word = (h < 32) ? m0 : m1;
+                        const bool b = ok && h < g.Hp && ((word >> (h & 31)) & 1u);
+                        const int r = (h < 32) ? __popc(m0 & ((1u << h) - 1u))
+                                               : c0 + __popc(m1 & ((1u << (h - 32)) - 1u));
+                        const int hc = min(max(h, g.pt), g.pt + g.H - 1);   // clamped: unconditional load
+                        const float val = pl0[t.z + hc * g.W];
+                        if (b) {
+                            dT[t.x + r] = val;
+                            if (win) iT[t.y + r] = Lc + h * g.S;
+                        }
+                    }
+                }
             } else if (NW <= 2) {
                 // two column items per warp iteration: table and mask loads of both in flight
                 for (int it0 = 2 * warp; it0 < nit; it0 += 2 * kEncWarps) {
