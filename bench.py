@@ -67,6 +67,16 @@ def nze_macs(d, x: np.ndarray, Oh, Ow) -> int:
     return int(ch @ nz @ cw) * d["K"]
 
 
+def tf32_peak():
+    """Dense TF32 tensor peak, TFLOP/s: the measured bf16 peak (MEASURED_PEAKS.json) times the
+    guide's nominal tf32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)."""
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["bf16_tflops"]) * 1.1 / 2.25
+    except Exception:
+        return 1100.0
+
+
 def load_peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -231,8 +241,12 @@ def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
         w_bytes = 4 * d["K"] * d["C"] * d["R"] * d["S"]
         if algo == "im2col":
             low = 4 * d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow
-            tr = max((x_bytes + 2 * low + w_bytes + y_bytes) / (hbm_gbs * 1e9),
-                     dense_flops(d, Oh, Ow) / (p_fp32 * 1e12))
+            if spc.spc_im2col_engine(d) == spc.SPC_GEMM_TC_3XTF32:
+                # three TF32 products per fp32 MAC at the TF32 tensor peak
+                t_mma = 3 * dense_flops(d, Oh, Ow) / (tf32_peak() * 1e12)
+            else:
+                t_mma = dense_flops(d, Oh, Ow) / (p_fp32 * 1e12)
+            tr = max((x_bytes + 2 * low + w_bytes + y_bytes) / (hbm_gbs * 1e9), t_mma)
         else:
             macs = nze_macs(dict(d, N=xb.shape[0]), xb, Oh, Ow) * reps * (d["N"] / (xb.shape[0] * reps))
             nnz = int((xb != 0).sum()) * d["N"] / xb.shape[0]
@@ -248,8 +262,13 @@ def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
            else "none (1 GPU)", "steps": args.stack_steps, "scaling": "strong (global batch fixed)",
            "roofline_images_per_s": (hi - lo) / t_roof if t_roof > 0 else None,
            "roofline_frac": (t_roof * 1e3) / t_tot if t_tot > 0 else None,
+           "roofline_model": "sum over layers of the chosen algorithm's bound: sparse = encode bytes / HBM + "
+                             "max(compressed + weight + output bytes / HBM, NZE FLOPs / FP32 peak); im2col = "
+                             "max(x + 2 x lowered + w + y bytes / HBM, dense FLOPs / FP32 peak (cuBLAS FP32) or "
+                             "3 x dense FLOPs / TF32 tensor peak (tcgen05 3xTF32))",
            "plan": layers, "select_ms_per_sample": S.select_times if rank == 0 else None,
            "gemm": spc.GEMM_NAMES[spc.spc_get_im2col_gemm()],
+           "gemm_per_layer": [spc.GEMM_NAMES[spc.spc_im2col_engine(sp["desc"])] for sp in S.specs],
            "inputs": "8 distinct seeded clustered-ReLU images per layer, tiled to the batch; L2 flushed per step"}
     if rank == 0 and not args.no_cpu:
         import oracle
@@ -430,7 +449,7 @@ def run_ours(args):
                          "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
                          "im2col_total": us(t_i2c)},
             "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
-                       "gemm": spc.GEMM_NAMES[spc.spc_get_im2col_gemm()]},
+                       "gemm": spc.GEMM_NAMES[spc.spc_im2col_engine(d)]},
             "speedup_vs_im2col": t_i2c / t_ms,
             "cr": {"cpo": cr_cpo, "cps": cr_cps, "cpo_with_side_tables": s_im2col / (pl_ + dl_ + il_ + side),
                    "ptr": pl_, "da": dl_, "in_cpo": il_, "in_cps": is_, "S_im2col": s_im2col},

@@ -135,14 +135,18 @@ spc_status spc_pack_weights(const spc_conv_desc *d, const float *w_kcrs, float *
 spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
                                float *y, int32_t fuse_relu, void *ws, size_t ws_bytes, void *stream);
 
-/* Dense baseline: im2col lowering of x into ws_lowered as
- * [N][C*R*S][Oh*Ow] fp32 (SI Eq. 6 elements), then a GEMM per image
- * y[n] = W[K x CRS] * L[n].  ws_bytes must be >= 4 * S_im2col. */
+/* Dense baseline: im2col lowering of x into ws_lowered (SI Eq. 6
+ * elements, fp32), then y[n] = W[K x CRS] * L[n].  Layout: [N][C*R*S][Oh*Ow] for the
+ * cuBLAS / SIMT engines, [N*Oh*Ow][C*R*S] (K-major, one GEMM over all images) for the
+ * tcgen05 engine.  ws_bytes must be >= 4 * S_im2col. */
 spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const float *w_kcrs, float *y,
                                int32_t fuse_relu, void *ws_lowered, size_t ws_bytes, void *stream);
 
 /* GEMM engines of the dense baseline.  im2col_conv_forward uses the process-wide
- * default (spc_set_im2col_gemm; initially SPC_GEMM_CUBLAS_FP32).  An engine the
+ * default (spc_set_im2col_gemm; initially SPC_GEMM_AUTO: the tcgen05 3xTF32 kernel for
+ * layers of >= 2^28 MACs with C*R*S % 4 == 0 (its TMA row pitches), cuBLAS FP32 otherwise,
+ * both within the 1e-4 tolerance).  SPC_GEMM_TC_3XTF32 also falls back to cuBLAS FP32
+ * when C*R*S % 4 != 0.  An engine the
  * loaded cuBLAS lacks makes im2col_conv_forward return SPC_EUNSUPPORTED (BF16X9
  * needs cuBLAS >= 12.9; PyTorch 2.11 bundles 12.8).  SPC_GEMM_SIMT is this library's own
  * FP32 FFMA kernel; the cuBLAS engines are plain library GEMMs (cublasGemmStridedBatchedEx):
@@ -152,10 +156,14 @@ spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const flo
  * reported for the crossover only). */
 typedef enum {
     SPC_GEMM_SIMT = 0, SPC_GEMM_CUBLAS_FP32 = 1, SPC_GEMM_CUBLAS_BF16X9 = 2, SPC_GEMM_CUBLAS_TF32 = 3,
-    SPC_GEMM_TC_3XTF32 = 4   /* this library's tcgen05 kernel: fp32 from three TF32 products, TMEM accumulators */
+    SPC_GEMM_TC_3XTF32 = 4,  /* this library's tcgen05 kernel: fp32 from three TF32 products, TMEM accumulators */
+    SPC_GEMM_AUTO = 5        /* TC_3XTF32 for large layers, CUBLAS_FP32 for small ones */
 } spc_gemm;
 spc_status spc_set_im2col_gemm(spc_gemm gemm);   /* SPC_EINVAL for an unknown engine */
 spc_gemm spc_get_im2col_gemm(void);
+/* The engine im2col_conv_forward runs for this layer under the current default (resolves
+ * SPC_GEMM_AUTO and the tcgen05 engine's C*R*S % 4 fallback); host only. */
+spc_gemm spc_im2col_engine(const spc_conv_desc *d);
 
 /* Host, synchronising (it times).  Per-layer offline selection:
  * over the M sample maps (device, M*N*C*H*W fp32), time encode+conv for CPO

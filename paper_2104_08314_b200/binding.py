@@ -75,18 +75,22 @@ _lib.spc_set_im2col_gemm.argtypes = [ctypes.c_int]
 _lib.spc_set_im2col_gemm.restype = ctypes.c_int
 _lib.spc_get_im2col_gemm.argtypes = []
 _lib.spc_get_im2col_gemm.restype = ctypes.c_int
+_lib.spc_im2col_engine.argtypes = [ctypes.c_void_p]
+_lib.spc_im2col_engine.restype = ctypes.c_int
 _lib.spc_select_ws_bytes.argtypes = [_D]
 _lib.spc_select_ws_bytes.restype = _sz
 _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
 EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
-                          "spc_get_im2col_gemm"]
+                          "spc_get_im2col_gemm", "spc_im2col_engine"]
 SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
+SPC_GEMM_AUTO = 5
 GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
               2: "cuBLAS FP32 emulated by 3 bf16 terms on tensor cores (CUBLAS_COMPUTE_32F_EMULATED_16BFX9)",
               3: "cuBLAS TF32 tensor cores (CUBLAS_COMPUTE_32F_FAST_TF32, 1 term)",
-              4: "tcgen05 3xTF32 (this library: fp32 from three TF32 products, TMEM accumulators)"}
+              4: "tcgen05 3xTF32 (this library: fp32 from three TF32 products, TMEM accumulators)",
+              5: "auto: tcgen05 3xTF32 for layers >= 2^28 MACs (C*R*S % 4 == 0), cuBLAS FP32 otherwise"}
 
 
 def spc_set_im2col_gemm(gemm: int) -> None:
@@ -97,6 +101,11 @@ def spc_set_im2col_gemm(gemm: int) -> None:
 
 def spc_get_im2col_gemm() -> int:
     return int(_lib.spc_get_im2col_gemm())
+
+
+def spc_im2col_engine(d: dict) -> int:
+    """The GEMM engine im2col_conv_forward runs for layer d (AUTO and fallbacks resolved)."""
+    return int(_lib.spc_im2col_engine(ctypes.byref(make_desc(d))))
 
 
 def _check(rc: int, where: str):

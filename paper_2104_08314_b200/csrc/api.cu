@@ -197,12 +197,17 @@ spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const flo
 }
 
 spc_status spc_set_im2col_gemm(spc_gemm gemm) {
-    if (gemm < SPC_GEMM_SIMT || gemm > SPC_GEMM_TC_3XTF32) return fail(SPC_EINVAL, "unknown GEMM engine %d", (int)gemm);
+    if (gemm < SPC_GEMM_SIMT || gemm > SPC_GEMM_AUTO) return fail(SPC_EINVAL, "unknown GEMM engine %d", (int)gemm);
     spc::set_gemm_engine((int)gemm);
     return SPC_OK;
 }
 
 spc_gemm spc_get_im2col_gemm(void) { return (spc_gemm)spc::gemm_engine(); }
+
+spc_gemm spc_im2col_engine(const spc_conv_desc* d) {
+    if (!d || check_desc(d) != SPC_OK) return spc_get_im2col_gemm();
+    return (spc_gemm)spc::gemm_engine_for(spc::make_geom(*d));
+}
 
 spc_status spc_encoding_lengths(const spc_encoding* enc, int64_t out_host[3], void* stream) {
     if (!enc || !enc->lengths || !out_host) return fail(SPC_EINVAL, "null pointer");

@@ -202,5 +202,6 @@ cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t 
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
 cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
 int gemm_engine();
+int gemm_engine_for(const Geom& g);   // effective engine of a layer (AUTO / fallbacks resolved)
 void set_gemm_engine(int e);
 }  // namespace spc

@@ -11,6 +11,16 @@
 
 namespace spc {
 
+static int g_gemm = SPC_GEMM_AUTO;   // im2col GEMM engine (spc_set_im2col_gemm)
+
+// The engine a layer actually runs: AUTO picks the tcgen05 kernel for large layers
+// (measured faster from cfg3 up: 66 vs 98 us; cfg2, 1.2e8 MACs: 31 vs 29 us for cuBLAS).
+static int effective_engine(const Geom& g) {
+    if (g_gemm != SPC_GEMM_AUTO) return g_gemm;
+    const double macs = (double)g.N * g.Oh * g.Ow * g.K * g.C * g.R * g.S;
+    return (macs >= 268435456.0) ? SPC_GEMM_TC_3XTF32 : SPC_GEMM_CUBLAS_FP32;
+}
+
 // Block (32, 8): threadIdx.x strides 32 consecutive output positions of a lowered row
 // (coalesced 128-byte stores), threadIdx.y picks one of 8 rows; rows = (n, c, l, m).
 __global__ void __launch_bounds__(256) im2col_kernel(Geom g, const float* __restrict__ x, float* __restrict__ L) {
@@ -46,7 +56,71 @@ __global__ void __launch_bounds__(256) im2col_row_kernel(Geom g, const float* __
     }
 }
 
+// K-major lowering for the tensor-core engine: A[m][crs] with m = n*P + p (one GEMM row per
+// image position, all images in one GEMM).  A block owns 32 positions x kTcCT tiles of 32
+// CRS; the per-CRS x offsets / tap rows and columns come from a table built once per block,
+// the per-position origin once per thread; 32 x 32 tiles go through shared memory so the
+// gathers from x (along output positions) and the stores (along CRS) are both coalesced.
+constexpr int kTcCT = 8;
+__global__ void __launch_bounds__(256) im2col_t_kernel(Geom g, const float* __restrict__ x, float* __restrict__ A) {
+    __shared__ float tile[32][33];
+    __shared__ int toff[32 * kTcCT];      // c*H*W + l*W + m - pt*W - pl
+    __shared__ short tl[32 * kTcCT], tm[32 * kTcCT];
+    const int P = g.Oh * g.Ow, RS = g.R * g.S, CRS = g.C * RS;
+    const long long M = (long long)g.N * P;
+    const long long m0 = (long long)blockIdx.x * 32;
+    const int kb0 = blockIdx.y * 32 * kTcCT;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < 32 * kTcCT; i += 256) {
+        const int crs = min(kb0 + i, CRS - 1);
+        const int c = crs / RS, rs = crs - c * RS, l = rs / g.S, mm = rs - l * g.S;
+        toff[i] = c * g.H * g.W + (l - g.pt) * g.W + (mm - g.pl);
+        tl[i] = (short)(l - g.pt);
+        tm[i] = (short)(mm - g.pl);
+    }
+    // this thread's load position (tx) and its origin in x
+    const long long ml = m0 + threadIdx.x;
+    const bool mok = ml < M;
+    const int n = mok ? (int)(ml / P) : 0, p = mok ? (int)(ml - (long long)n * P) : 0;
+    const int oy = p / g.Ow, ox = p - oy * g.Ow;
+    const int hy = oy * g.sh, wx = ox * g.sw;
+    const float* xn = x + (long long)n * g.C * g.H * g.W + hy * g.W + wx;
+    __syncthreads();
+    for (int t = 0; t < kTcCT; t++) {
+        const int k0 = kb0 + 32 * t;
+        if (k0 >= CRS) break;
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int i = 32 * t + threadIdx.y + 8 * u;
+            const int h = hy + tl[i], w = wx + tm[i];
+            const bool ok = mok && k0 + threadIdx.y + 8 * u < CRS && h >= 0 && h < g.H && w >= 0 && w < g.W;
+            v[u] = ok ? __ldg(xn + toff[i]) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) tile[threadIdx.y + 8 * u][threadIdx.x] = v[u];
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const long long m = m0 + threadIdx.y + 8 * u;
+            const int crs = k0 + threadIdx.x;
+            if (m < M && crs < CRS) A[m * CRS + crs] = tile[threadIdx.x][threadIdx.y + 8 * u];
+        }
+        __syncthreads();
+    }
+}
+
+// The tensor-core engine runs when TMA can address the operands (CRS % 4 == 0: 16-byte row
+// pitches); other shapes fall back to cuBLAS FP32 with the standard lowering.
+bool tc_layout(const Geom& g) { return effective_engine(g) == SPC_GEMM_TC_3XTF32 && (g.C * g.R * g.S) % 4 == 0; }
+
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st) {
+    if (tc_layout(g)) {
+        const long long M = (long long)g.N * g.Oh * g.Ow;
+        const int crs = g.C * g.R * g.S;
+        im2col_t_kernel<<<dim3((unsigned)((M + 31) / 32), (crs + 32 * kTcCT - 1) / (32 * kTcCT)), dim3(32, 8), 0, st>>>(g, x, L);
+        return cudaGetLastError();
+    }
     const long long rows = (long long)g.N * g.C * g.R * g.S;
     const int P = g.Oh * g.Ow;
     if (P >= 512) {
@@ -151,9 +225,12 @@ __global__ void relu_kernel(float* y, long long n) {
         y[i] = fmaxf(y[i], 0.f);
 }
 
-static int g_gemm = SPC_GEMM_CUBLAS_FP32;
 
 int gemm_engine() { return g_gemm; }
+int gemm_engine_for(const Geom& g) {
+    const int e = effective_engine(g);
+    return (e == SPC_GEMM_TC_3XTF32 && (g.C * g.R * g.S) % 4 != 0) ? SPC_GEMM_CUBLAS_FP32 : e;
+}
 void set_gemm_engine(int e) { g_gemm = e; }
 
 // one cuBLAS handle per device, created on first use (cuBLAS calls are stream-ordered
@@ -196,8 +273,12 @@ static cudaError_t cublas_gemm(const Geom& g, const float* w, const float* L, fl
 }
 
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st) {
-    if (g_gemm == SPC_GEMM_TC_3XTF32) return launch_tc_gemm(g, w, L, y, relu, st);
-    if (g_gemm != SPC_GEMM_SIMT) return cublas_gemm(g, w, L, y, relu, st, g_gemm);
+    const int eng = effective_engine(g);
+    if (eng == SPC_GEMM_TC_3XTF32) {
+        if (tc_layout(g)) return launch_tc_gemm(g, w, L, y, relu, st);
+        return cublas_gemm(g, w, L, y, relu, st, SPC_GEMM_CUBLAS_FP32);
+    }
+    if (eng != SPC_GEMM_SIMT) return cublas_gemm(g, w, L, y, relu, st, eng);
     const int M = g.K, N = g.Oh * g.Ow, Kd = g.C * g.R * g.S;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, g.N);
     sgemm_kernel<<<grid, 256, 0, st>>>(M, N, Kd, w, L, (long long)Kd * N, y, (long long)M * N, relu);

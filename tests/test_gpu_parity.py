@@ -318,12 +318,14 @@ def test_im2col_tf32_engine_runs():
 
 
 @pytest.mark.parametrize("shape", [(1, 64, 56, 56, 64, 1), (2, 256, 14, 14, 256, 1), (2, 128, 28, 28, 128, 2),
-                                   (1, 5, 9, 11, 70, 1), (2, 3, 17, 17, 33, 1), (3, 512, 7, 7, 512, 1)])
+                                   (1, 5, 9, 11, 70, 1), (2, 3, 17, 17, 33, 1), (3, 512, 7, 7, 512, 1),
+                                   (3, 4, 9, 11, 70, 1), (5, 8, 13, 10, 200, 2)])
 def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
-    """tcgen05 3xTF32 baseline GEMM vs the FP64 oracle on ragged shapes (P, K, CRS not tile multiples).
-    Up to CRS = 2304 it meets the north_star tolerance; at CRS = 4608 (512 channels) the tensor-core
-    accumulation of the three TF32 products leaves ~2e-5 absolute error on near-zero outputs, so
-    there the bound is 1e-4 of the output scale (the parity-passing default is cuBLAS FP32)."""
+    """tcgen05 3xTF32 baseline GEMM vs the FP64 oracle on ragged shapes (P, K, CRS not tile
+    multiples; CRS % 4 != 0 runs the cuBLAS FP32 fallback).  The TMEM accumulator is drained into
+    fp32 register sums every 256 CRS, which keeps CRS = 4608 (512 channels) inside the strict
+    north_star tolerance too (one tensor-core accumulation over all of CRS left ~2e-5 absolute
+    error on near-zero outputs)."""
     N, C, H, W, K, s = shape
     d = layer_desc(N, C, H, W, K, 3, 3, s, s, 1, 1, 1, 1)
     x = clustered_relu(N, C, H, W, 0.3, 11)
@@ -336,8 +338,4 @@ def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
         got = L.im2col(torch.from_numpy(x).cuda()).cpu().numpy()
     finally:
         spc.spc_set_im2col_gemm(prev)
-    if C * 9 <= 2304:
-        _check_conv(got, ref, f"tc 3xtf32 {shape}")
-    else:
-        err = np.abs(got - ref).max()
-        assert err <= 1e-4 * np.abs(ref).max(), f"tc 3xtf32 {shape}: max abs err {err}"
+    _check_conv(got, ref, f"tc 3xtf32 {shape}")

@@ -67,7 +67,7 @@ def main():
         for name, e in engines.items():
             spc.spc_set_im2col_gemm(e)
             t_dense[name] = timed(L.capture(lambda: L.forward(x0, "im2col")))
-        spc.spc_set_im2col_gemm(spc.SPC_GEMM_CUBLAS_FP32)
+        spc.spc_set_im2col_gemm(spc.SPC_GEMM_AUTO)
         rows = []
         s_i2c = d["N"] * L.Oh * L.Ow * d["C"] * d["R"] * d["S"]
         for rho in RHOS:
