@@ -57,56 +57,67 @@ __global__ void __launch_bounds__(256) im2col_row_kernel(Geom g, const float* __
 }
 
 // K-major lowering for the tensor-core engine: A[m][crs] with m = n*P + p (one GEMM row per
-// image position, all images in one GEMM).  A block owns 32 positions x kTcCT tiles of 32
-// CRS; the per-CRS x offsets / tap rows and columns come from a table built once per block,
-// the per-position origin once per thread; 32 x 32 tiles go through shared memory so the
-// gathers from x (along output positions) and the stores (along CRS) are both coalesced.
-constexpr int kTcCT = 8;
-__global__ void __launch_bounds__(256) im2col_t_kernel(Geom g, const float* __restrict__ x, float* __restrict__ A) {
-    __shared__ float tile[32][33];
-    __shared__ int toff[32 * kTcCT];      // c*H*W + l*W + m - pt*W - pl
-    __shared__ short tl[32 * kTcCT], tm[32 * kTcCT];
-    const int P = g.Oh * g.Ow, RS = g.R * g.S, CRS = g.C * RS;
+// image position, all images in one GEMM).  A block owns 32 positions x kTcCB input channels:
+// warps read x with lanes along the positions (coalesced; tap offsets by increment, no
+// divisions) into a column-major smem tile, then write each position's C*R*S slice with
+// lanes along CRS (coalesced 128-byte rows).  The tile is [CB*R*S][33] so both phases are
+// bank-conflict free.
+constexpr int kTcCB = 32;
+template <int R_, int S_>   // compile-time taps (all loads of a channel in flight), or 0, 0: runtime
+__global__ void __launch_bounds__(256) im2col_t_kernel(Geom g, const float* __restrict__ x, float* __restrict__ A,
+                                                       int cb) {
+    extern __shared__ float tile[];               // [cb * RS][33]
+    const int R = R_ ? R_ : g.R, S = S_ ? S_ : g.S;
+    const int P = g.Oh * g.Ow, RS = R * S, CRS = g.C * RS;
     const long long M = (long long)g.N * P;
     const long long m0 = (long long)blockIdx.x * 32;
-    const int kb0 = blockIdx.y * 32 * kTcCT;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    for (int i = tid; i < 32 * kTcCT; i += 256) {
-        const int crs = min(kb0 + i, CRS - 1);
-        const int c = crs / RS, rs = crs - c * RS, l = rs / g.S, mm = rs - l * g.S;
-        toff[i] = c * g.H * g.W + (l - g.pt) * g.W + (mm - g.pl);
-        tl[i] = (short)(l - g.pt);
-        tm[i] = (short)(mm - g.pl);
+    const int c0 = blockIdx.y * cb;
+    const int nc = min(cb, g.C - c0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        const long long m = m0 + lane;
+        const bool mok = m < M;
+        const int n = mok ? (int)(m / P) : 0, p = mok ? (int)(m - (long long)n * P) : 0;
+        const int oy = p / g.Ow, ox = p - oy * g.Ow;
+        const int h0 = oy * g.sh - g.pt, w0 = ox * g.sw - g.pl;
+#pragma unroll 4
+        for (int ci = warp; ci < nc; ci += 8) {
+            const float* xc = x + ((long long)n * g.C + c0 + ci) * g.H * g.W;
+            float* tc = tile + ci * RS * 33 + lane;
+            if constexpr (R_ > 0) {
+                float v[R_ * S_];
+#pragma unroll
+                for (int l = 0; l < R_; l++) {
+                    const int h = h0 + l;
+                    const bool hok = mok && h >= 0 && h < g.H;
+#pragma unroll
+                    for (int mm = 0; mm < S_; mm++) {
+                        const int w = w0 + mm;
+                        v[l * S_ + mm] = (hok && w >= 0 && w < g.W) ? __ldg(xc + h * g.W + w) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < R_ * S_; t++) tc[t * 33] = v[t];
+            } else {
+                int t = 0;
+                for (int l = 0; l < R; l++) {
+                    const int h = h0 + l;
+                    const bool hok = mok && h >= 0 && h < g.H;
+                    for (int mm = 0; mm < S; mm++, t++) {
+                        const int w = w0 + mm;
+                        tc[t * 33] = (hok && w >= 0 && w < g.W) ? __ldg(xc + h * g.W + w) : 0.f;
+                    }
+                }
+            }
+        }
     }
-    // this thread's load position (tx) and its origin in x
-    const long long ml = m0 + threadIdx.x;
-    const bool mok = ml < M;
-    const int n = mok ? (int)(ml / P) : 0, p = mok ? (int)(ml - (long long)n * P) : 0;
-    const int oy = p / g.Ow, ox = p - oy * g.Ow;
-    const int hy = oy * g.sh, wx = ox * g.sw;
-    const float* xn = x + (long long)n * g.C * g.H * g.W + hy * g.W + wx;
     __syncthreads();
-    for (int t = 0; t < kTcCT; t++) {
-        const int k0 = kb0 + 32 * t;
-        if (k0 >= CRS) break;
-        float v[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int i = 32 * t + threadIdx.y + 8 * u;
-            const int h = hy + tl[i], w = wx + tm[i];
-            const bool ok = mok && k0 + threadIdx.y + 8 * u < CRS && h >= 0 && h < g.H && w >= 0 && w < g.W;
-            v[u] = ok ? __ldg(xn + toff[i]) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) tile[threadIdx.y + 8 * u][threadIdx.x] = v[u];
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const long long m = m0 + threadIdx.y + 8 * u;
-            const int crs = k0 + threadIdx.x;
-            if (m < M && crs < CRS) A[m * CRS + crs] = tile[threadIdx.x][threadIdx.y + 8 * u];
-        }
-        __syncthreads();
+    const int row = nc * RS;
+    for (int pp = warp; pp < 32; pp += 8) {
+        const long long m = m0 + pp;
+        if (m >= M) break;
+        float* dst = A + m * CRS + (long long)c0 * RS;
+        for (int col = lane; col < row; col += 32) dst[col] = tile[col * 33 + pp];
     }
 }
 
@@ -117,8 +128,17 @@ bool tc_layout(const Geom& g) { return effective_engine(g) == SPC_GEMM_TC_3XTF32
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st) {
     if (tc_layout(g)) {
         const long long M = (long long)g.N * g.Oh * g.Ow;
-        const int crs = g.C * g.R * g.S;
-        im2col_t_kernel<<<dim3((unsigned)((M + 31) / 32), (crs + 32 * kTcCT - 1) / (32 * kTcCT)), dim3(32, 8), 0, st>>>(g, x, L);
+        const int RS = g.R * g.S;
+        const int cb = std::max(1, std::min(kTcCB, 320 / RS));     // tile <= 320 x 33 floats (42 KB)
+        const size_t smem = (size_t)cb * RS * 33 * sizeof(float);
+        auto kern = (g.R == 3 && g.S == 3) ? im2col_t_kernel<3, 3>
+                  : (g.R == 1 && g.S == 7) ? im2col_t_kernel<1, 7>
+                  : (g.R == 7 && g.S == 1) ? im2col_t_kernel<7, 1> : im2col_t_kernel<0, 0>;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<dim3((unsigned)((M + 31) / 32), (g.C + cb - 1) / cb), 256, smem, st>>>(g, x, L, cb);
         return cudaGetLastError();
     }
     const long long rows = (long long)g.N * g.C * g.R * g.S;

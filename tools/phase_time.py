@@ -39,7 +39,8 @@ def main():
     for wl in sys.argv[1:]:
         c = workload(wl)
         d = c["desc"]
-        x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"] or 0.3, c["seed"], c["dead_frac"], c["zero_tile_frac"])
+        rho = float(os.environ["PHASE_DENSITY"]) if os.environ.get("PHASE_DENSITY") else (c["density"] or 0.3)
+        x = clustered_relu(d["N"], d["C"], d["H"], d["W"], rho, c["seed"], c["dead_frac"], c["zero_tile_frac"])
         w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
         L = SparseConvLayer(d, torch.from_numpy(w).cuda())
         L.encode(torch.from_numpy(x).cuda(), "cpo")
