@@ -76,3 +76,27 @@ def test_binding_refuses_cpu_tensors(lib):
     d = _d()
     with pytest.raises(ValueError):
         lib.binding._ptr(torch.zeros(4))
+
+
+def test_im2col_engine_resolution(lib):
+    """SPC_GEMM_AUTO (the default) picks the tcgen05 3xTF32 kernel for layers of >= 2^28 MACs
+    whose C*R*S is a multiple of 4 (TMA row pitches), cuBLAS FP32 otherwise; an explicit
+    TC_3XTF32 falls back to cuBLAS FP32 when C*R*S % 4 != 0 (include/spconv.h)."""
+    prev = lib.spc_get_im2col_gemm()
+    try:
+        lib.spc_set_im2col_gemm(lib.SPC_GEMM_AUTO)
+        big = _d(N=32, C=64, H=56, W=56, K=64)            # 3.7e9 MACs, CRS = 576
+        small = _d(N=1, C=64, H=56, W=56, K=64)           # cfg2: 1.2e8 MACs
+        odd = _d(N=32, C=65, H=56, W=56, K=64)            # CRS = 585
+        assert lib.spc_im2col_engine(big) == lib.SPC_GEMM_TC_3XTF32
+        assert lib.spc_im2col_engine(small) == lib.SPC_GEMM_CUBLAS_FP32
+        assert lib.spc_im2col_engine(odd) == lib.SPC_GEMM_CUBLAS_FP32
+        lib.spc_set_im2col_gemm(lib.SPC_GEMM_TC_3XTF32)
+        assert lib.spc_im2col_engine(small) == lib.SPC_GEMM_TC_3XTF32
+        assert lib.spc_im2col_engine(odd) == lib.SPC_GEMM_CUBLAS_FP32
+        lib.spc_set_im2col_gemm(lib.SPC_GEMM_SIMT)
+        assert lib.spc_im2col_engine(big) == lib.SPC_GEMM_SIMT
+        with pytest.raises(lib.SpcError):
+            lib.spc_set_im2col_gemm(6)
+    finally:
+        lib.spc_set_im2col_gemm(prev)

@@ -275,7 +275,7 @@ def test_select_layer_algo_argmin():
 
 
 @pytest.mark.parametrize("engine", [spc.SPC_GEMM_SIMT, spc.SPC_GEMM_CUBLAS_FP32, spc.SPC_GEMM_CUBLAS_BF16X9,
-                                    spc.SPC_GEMM_TC_3XTF32])
+                                    spc.SPC_GEMM_TC_3XTF32, spc.SPC_GEMM_AUTO])
 def test_im2col_gemm_engines_within_tolerance(oracle_mod, engine):
     """Every dense-baseline GEMM engine that the selector may use meets the fp32 tolerance."""
     c = CONFIGS["cfg3"]
