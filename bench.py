@@ -33,7 +33,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth import CONFIGS, cfg5_layers, clustered_relu, he_normal  # noqa: E402
+from synth import CATALOG, CONFIGS, cfg5_layers, clustered_relu, he_normal  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT, FP32_LANES, FALLBACK_HBM = 148, 128, 6650.0
@@ -44,6 +44,8 @@ def workload(name: str):
     if name.startswith("cfg5"):
         layer = cfg5_layers(batch=32)[int(name.split("L")[-1])]
         return layer
+    if name in CATALOG:
+        return CATALOG[name]
     return CONFIGS[name]
 
 

@@ -1259,11 +1259,11 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const StripPlan<T> pl = plan_strip<T>(g);
     const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
     a.rt = pl.rt;
-    if (a.rt > T::MAXW) return cudaErrorInvalidValue;
+    if (a.rt > T::MAXW) return cudaErrorNotSupported;          // the generic kernel runs instead
     a.csplit = pl.csplit;
     a.cg = cg;
     const size_t smem = strip_smem<T>(a);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    if (smem > 227 * 1024) return cudaErrorNotSupported;      // (very wide maps: long ptr segments)
     // Balanced mode when the units outnumber the SMs and the busiest SM would get >= 20%
     // more units than the average (a CTA's time changes little with a second co-resident
     // CTA, so the SM holding the most units sets the kernel time): one CTA per resident
@@ -1302,6 +1302,13 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
         if (g.K <= 64 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32, true>{});
         if (g.Oh <= 32) return f(StripCfg<3, 3, 1, 1, 4, 4, 4>{});
         if (g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 4, 1>{});
+        if (g.Oh <= 128) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 16, true>{});   // up to 16 row tiles
+    } else if (g.R == 5 && g.S == 5 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
+        return f(StripCfg<5, 5, 1, 1, 4, 4, 2, 1, 16, 16>{});
+    } else if (g.R == 1 && g.S == 3 && g.sh == 1 && g.sw == 1 && g.Oh <= 32) {
+        return f(StripCfg<1, 3, 1, 1, 4, 4, 4>{});
+    } else if (g.R == 3 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 32) {
+        return f(StripCfg<3, 1, 1, 1, 4, 4, 4>{});
     } else if (g.R == 3 && g.S == 3 && g.sh == 2 && g.sw == 2) {
         if (g.K <= 64 && g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 2>{});
         if (g.Oh <= 16) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>{});

@@ -7,4 +7,4 @@ workload catalogue (shapes, pads, strides, densities, seeds).  See
 DESIGN.md "Input recipe" and SURVEY.md Appendix B.
 """
 from .gen import clustered_relu, he_normal, int_map, int_weights, random_sparse  # noqa: F401
-from .configs import CONFIGS, cfg5_layers, layer_desc  # noqa: F401
+from .configs import CATALOG, CONFIGS, cfg5_layers, layer_desc  # noqa: F401

@@ -42,6 +42,24 @@ CONFIGS = {
                   note="input = ReLU(cfg4a output)"),
 }
 
+# Shape catalog beyond the BASELINE configs (SURVEY.md §8(f) NEXT-4 "shape sweeps"): the
+# non-pointwise layer shapes of the paper's other CNNs -- Inception-v3 (5x5 and 3x3 at 35x35,
+# 1x7 / 7x1 at 17x17 with 128 / 160 channels, 1x3 / 3x1 at 8x8) and a VGG-style 3x3 at
+# 112x112 (outside the strip kernel's row range: the generic kernel).  Synthetic inputs as
+# cfg3/cfg4 (clustered ReLU, batch 8, He weights); crossover sweeps only (tools/crossover.py).
+CATALOG = {
+    "iv3_5x5_35": dict(desc=layer_desc(8, 48, 35, 35, 64, 5, 5, 1, 1, 2, 2, 2, 2), density=0.3, seed=201),
+    "iv3_3x3_35": dict(desc=layer_desc(8, 64, 35, 35, 96, 3, 3, 1, 1, 1, 1, 1, 1), density=0.3, seed=202),
+    "iv3_3x3_35b": dict(desc=layer_desc(8, 96, 35, 35, 96, 3, 3, 1, 1, 1, 1, 1, 1), density=0.3, seed=203),
+    "iv3_1x7_17": dict(desc=layer_desc(8, 128, 17, 17, 128, 1, 7, 1, 1, 0, 0, 3, 3), density=0.3, seed=204),
+    "iv3_7x1_17": dict(desc=layer_desc(8, 160, 17, 17, 160, 7, 1, 1, 1, 3, 3, 0, 0), density=0.3, seed=205),
+    "iv3_1x3_8": dict(desc=layer_desc(8, 384, 8, 8, 384, 1, 3, 1, 1, 0, 0, 1, 1), density=0.3, seed=206),
+    "iv3_3x1_8": dict(desc=layer_desc(8, 384, 8, 8, 384, 3, 1, 1, 1, 1, 1, 0, 0), density=0.3, seed=207),
+    "vgg_3x3_112": dict(desc=layer_desc(1, 128, 112, 112, 128, 3, 3, 1, 1, 1, 1, 1, 1), density=0.3, seed=208),
+}
+for _c in CATALOG.values():
+    _c.update(dead_frac=0.0, zero_tile_frac=0.0)
+
 # ResNet-50 v1.5 non-pointwise 3x3 layers (C_in == C_out), all pad 1.
 _CFG5 = ([(64, 56, 1)] * 3 + [(128, 56, 2)] + [(128, 28, 1)] * 3 +
          [(256, 28, 2)] + [(256, 14, 1)] * 5 + [(512, 14, 2)] + [(512, 7, 1)] * 2)

@@ -138,6 +138,18 @@ def test_cfg5_layers_sampled(oracle_mod, li):
     _layer_case(oracle_mod, d, x, w, full=False, samples=3000, seed=li)
 
 
+@pytest.mark.parametrize("name", ["iv3_5x5_35", "iv3_1x3_8", "iv3_7x1_17", "vgg_3x3_112"])
+def test_catalog_shapes_sampled(oracle_mod, name):
+    """Shape-catalog layers (5x5, 1x3, 7x1 kernels; a 112x112 map on the generic kernel):
+    encodings bit-exact, sampled outputs of CPO / CPS / im2col within tolerance."""
+    from synth import CATALOG
+    c = CATALOG[name]
+    d = c["desc"]
+    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"])
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
+    _layer_case(oracle_mod, d, x, w, full=False, samples=2000, seed=c["seed"])
+
+
 @pytest.mark.parametrize("shape", [(48, 64, 56, 56), (96, 128, 28, 28)])
 def test_encoder_multi_round_tiles(oracle_mod, shape):
     """Batches whose tiles outnumber the resident CTAs (the cfg5 stack at batch 256 on one
