@@ -1313,6 +1313,7 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
         if (g.K <= 64 && g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 2>{});
         if (g.Oh <= 16) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 16>{});
         if (g.Oh <= 32) return f(StripCfg<3, 3, 2, 2, 4, 4, 4, 2, 8, 8>{});   // 8: keeps 2 CTAs/SM
+        if (g.Oh <= 64) return f(StripCfg<3, 3, 2, 2, 4, 4, 2, 1, 16, 16>{});  // up to 16 row tiles
     } else if (g.R == 1 && g.S == 7 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
         return f(StripCfg<1, 7, 1, 1, 8, 4, 2, 2, 8, 16, true>{});
     } else if (g.R == 7 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {

@@ -56,6 +56,7 @@ CATALOG = {
     "iv3_1x3_8": dict(desc=layer_desc(8, 384, 8, 8, 384, 1, 3, 1, 1, 0, 0, 1, 1), density=0.3, seed=206),
     "iv3_3x1_8": dict(desc=layer_desc(8, 384, 8, 8, 384, 3, 1, 1, 1, 1, 1, 0, 0), density=0.3, seed=207),
     "vgg_3x3_112": dict(desc=layer_desc(1, 128, 112, 112, 128, 3, 3, 1, 1, 1, 1, 1, 1), density=0.3, seed=208),
+    "s2_3x3_112": dict(desc=layer_desc(2, 128, 112, 112, 128, 3, 3, 2, 2, 1, 1, 1, 1), density=0.3, seed=209),
 }
 for _c in CATALOG.values():
     _c.update(dead_frac=0.0, zero_tile_frac=0.0)

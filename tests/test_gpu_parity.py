@@ -138,7 +138,7 @@ def test_cfg5_layers_sampled(oracle_mod, li):
     _layer_case(oracle_mod, d, x, w, full=False, samples=3000, seed=li)
 
 
-@pytest.mark.parametrize("name", ["iv3_5x5_35", "iv3_1x3_8", "iv3_7x1_17", "vgg_3x3_112"])
+@pytest.mark.parametrize("name", ["iv3_5x5_35", "iv3_1x3_8", "iv3_7x1_17", "vgg_3x3_112", "s2_3x3_112"])
 def test_catalog_shapes_sampled(oracle_mod, name):
     """Shape-catalog layers (5x5, 1x3, 7x1 kernels; a 112x112 map on the generic kernel):
     encodings bit-exact, sampled outputs of CPO / CPS / im2col within tolerance."""
