@@ -186,6 +186,44 @@ def test_balanced_mode_full(oracle_mod, shape, capfd, monkeypatch):
     _check_conv(L.conv(relu=True).cpu().numpy(), np.maximum(ref, 0.0), "balanced mode + relu")
 
 
+def _stream_slice(enc_gpu, c0, c1):
+    """GPU streams of channels [c0, c1) (global n*C + c indices) with offsets rebased to 0."""
+    cp, cz, ci = (enc_gpu[k].astype(np.int64) for k in ("chan_ptr_off", "chan_nz_off", "chan_in_off"))
+    return dict(ptr=enc_gpu["ptr"][cp[c0]:cp[c1]], da=enc_gpu["da"][cz[c0]:cz[c1]], inn=enc_gpu["inn"][ci[c0]:ci[c1]],
+                chan_ptr_off=cp[c0:c1 + 1] - cp[c0], chan_nz_off=cz[c0:c1 + 1] - cz[c0],
+                chan_in_off=ci[c0:c1 + 1] - ci[c0])
+
+
+@pytest.mark.parametrize("li", [0, 8])
+def test_stack_layer_full_batch(oracle_mod, li):
+    """A cfg5 layer at the stack's full per-GPU batch (256 images, the size bench.py times at
+    N = 1: multi-round encoder tiles, the tcgen05 GEMM over 256 x P rows).  Streams bit-exact
+    for the first and the last two images (the tail checks the prefix sums at the end of the
+    long stream); sampled outputs of CPO and im2col within tolerance over all 256 images."""
+    from paper_2104_08314_b200.stack import tile_images
+    layer = cfg5_layers(batch=256)[li]
+    d = layer["desc"]
+    base = clustered_relu(8, d["C"], d["H"], d["W"], layer["density"], layer["seed"])
+    x = tile_images(base, 256)
+    w = he_normal(d["K"], d["C"], d["R"], d["S"], layer["seed"])
+    xg = torch.from_numpy(x).cuda()
+    L = GpuLayer(d, w)
+    L.encode(xg)
+    got = L.streams()
+    C = d["C"]
+    for n0 in (0, 254):        # images 254, 255 repeat base images 6, 7
+        d2 = dict(d, N=2)
+        ref = oracle_mod.encode(d2, base[n0 % 8:n0 % 8 + 2])
+        assert_streams_equal(_stream_slice(got, n0 * C, (n0 + 2) * C), ref, f"images {n0}, {n0 + 1}")
+    y_cpo = L.conv().cpu().numpy()
+    y_i2c = L.im2col(xg).cpu().numpy()
+    rng = np.random.default_rng(li)
+    idx = np.stack([rng.integers(0, s, 3000) for s in y_cpo.shape], axis=1)
+    ref = oracle_mod.direct_conv_at(d, x, w, idx)
+    for name, y in (("cpo", y_cpo), ("im2col", y_i2c)):
+        _check_conv(y[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]], ref, f"L{li} batch 256 {name}")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _desc3(**kw):
