@@ -228,18 +228,79 @@ __device__ __forceinline__ void column_range_s(const Geom& g, const int32_t* seg
 // patterns alternate, so a lane knows its role from the distance to the last
 // negative entry (carried across 32-entry chunks); per-entry NZE counts
 // (1 / popc(P) / 0) are scanned to give each entry its DA position.
+// One CTA per channel: the block's entries are cut into 8 warp segments; a warp finds
+// its starting role by looking back to the last negative entry before its segment,
+// counts its NZEs (pass 1), takes its DA base from a scan over the warps' counts, and
+// writes (pass 2, loads served by L1).
 // Output: CPO-form indices at DA positions (in_cpo[chan_nz_off + r]).
+template <bool WRITE>
+__device__ __forceinline__ int cps_segment(const int32_t* __restrict__ in, long long Q, int q0, int q1, int nin,
+                                           bool carry_pat, int S, int32_t* __restrict__ out, long long obase) {
+    const int lane = threadIdx.x & 31;
+    int dpos = 0;
+    constexpr int B = 4;     // chunks of 32 entries whose loads are in flight together
+    for (int q = q0; q < q1; q += 32 * B) {
+        int eb[B];
+#pragma unroll
+        for (int b = 0; b < B; b++) {
+            const int i = q + 32 * b + lane;
+            eb[b] = (i < q1) ? __ldg(in + Q + i) : -1;
+        }
+        const int after = min(q + 32 * B, q1);                      // first entry after the batch
+        const int tail = (after < nin) ? __ldg(in + Q + after) : -1;
+#pragma unroll
+        for (int b = 0; b < B; b++) {
+            const int i = q + 32 * b + lane;
+            const bool valid = i < q1;
+            const int e = eb[b];
+            const unsigned neg = __ballot_sync(0xffffffffu, valid && e < 0);
+            const unsigned before = neg & lanemask_lt();
+            const int r = before ? (32 - __clz(before)) : 0;  // run start (lane after the last negative)
+            const bool base_pat = (r == 0) ? carry_pat : false;
+            const bool is_pat = valid && e >= 0 && (base_pat ^ (((lane - r) & 1) != 0));
+            const bool is_idx = valid && e >= 0 && !is_pat;
+            int nxt = __shfl_down_sync(0xffffffffu, e, 1);
+            // the successor of the last valid entry of the chunk: lane 0 of the next chunk,
+            // or the entry after the batch (the next segment's first entry)
+            const int first_next = __shfl_sync(0xffffffffu, (b + 1 < B) ? eb[(b + 1) % B] : tail, 0);
+            const bool next_in_batch = (b + 1 < B) && (q + 32 * (b + 1) < q1);
+            if (lane == 31) nxt = next_in_batch ? first_next : tail;
+            if (valid && i + 1 == q1) nxt = tail;                    // last entry of the segment
+            const int cnt = !valid ? 0 : (e < 0 ? 1 : (is_idx ? __popc(nxt & 0xF) : 0));
+            int tot;
+            const int ex = warp_exclusive_scan(cnt, &tot);
+            if (WRITE) {
+                const long long o = obase + dpos + ex;
+                if (valid && e < 0) {
+                    out[o] = -e;
+                } else if (is_idx) {
+                    const unsigned p = (unsigned)nxt & 0xFu;
+                    const int b0 = __ffs(p) - 1;
+                    int u = 0;
+#pragma unroll
+                    for (int bb = 0; bb < 4; bb++)
+                        if ((p >> bb) & 1u) out[o + u++] = e + S * (bb - b0);
+                }
+            }
+            carry_pat = __shfl_sync(0xffffffffu, is_idx, 31);
+            dpos += tot;
+            if (q + 32 * (b + 1) >= q1) break;
+        }
+    }
+    return dpos;
+}
+
 __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* __restrict__ ptr,
                                                          const int32_t* __restrict__ in,
                                                          const int64_t* __restrict__ cpo_off,
                                                          const int64_t* __restrict__ cnz_off,
                                                          const int64_t* __restrict__ cin_off,
                                                          int32_t* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const long long nc = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    __shared__ int s_cnt[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long nc = blockIdx.x;
     pdl_wait();
     pdl_trigger();
-    if (nc >= g.NC) return;
     const long long Z = cnz_off[nc], Q = cin_off[nc];
     const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q);
     if (nnz == 0) return;
@@ -250,62 +311,35 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
         dmid = (d.pos[g.S - 1] >= 0) ? d.da[g.S - 1] : nnz;
     }
     // 1:1 part (every block below overlapK_w; all of it for S = 1)
-    for (int r = lane; r < dmid; r += 32) out[Z + r] = in[Q + r];
+    for (int r = threadIdx.x; r < dmid; r += blockDim.x) out[Z + r] = in[Q + r];
     if (dmid == nnz) return;
-    const int S = g.S;
-    int q = dmid, dpos = dmid;
-    bool carry_pat = false;  // next entry is a pattern (its index ended the previous chunk)
-    constexpr int B = 8;     // chunks of 32 entries whose loads are in flight together
-    while (q < nin) {
-        int eb[B];
-#pragma unroll
-        for (int b = 0; b < B; b++) {
-            const int i = q + 32 * b + lane;
-            eb[b] = (i < nin) ? __ldg(in + Q + i) : -1;
-        }
-        const int tail = (q + 32 * B < nin) ? __ldg(in + Q + q + 32 * B) : -1;   // first entry after the batch
-#pragma unroll
-        for (int b = 0; b < B; b++) {
-            const int i = q + 32 * b + lane;
-            const bool valid = i < nin;
-            const int e = eb[b];
-            const unsigned neg = __ballot_sync(0xffffffffu, valid && e < 0);
-            const unsigned before = neg & lanemask_lt();
-            const int r = before ? (32 - __clz(before)) : 0;  // run start (lane after the last negative)
-            const bool base_pat = (r == 0) ? carry_pat : false;
-            const bool is_pat = valid && e >= 0 && (base_pat ^ (((lane - r) & 1) != 0));
-            const bool is_idx = valid && e >= 0 && !is_pat;
-            int nxt = __shfl_down_sync(0xffffffffu, e, 1);
-            // lane 31's successor is lane 0 of the next chunk (or the entry after the batch)
-            const int first_next = __shfl_sync(0xffffffffu, (b + 1 < B) ? eb[(b + 1) % B] : tail, 0);
-            if (lane == 31) nxt = (b + 1 < B) ? first_next : tail;
-            const int cnt = !valid ? 0 : (e < 0 ? 1 : (is_idx ? __popc(nxt & 0xF) : 0));
-            int tot;
-            const int ex = warp_exclusive_scan(cnt, &tot);
-            const long long o = Z + dpos + ex;
-            if (valid && e < 0) {
-                out[o] = -e;
-            } else if (is_idx) {
-                const unsigned p = (unsigned)nxt & 0xFu;
-                const int b0 = __ffs(p) - 1;
-                int u = 0;
-#pragma unroll
-                for (int bb = 0; bb < 4; bb++)
-                    if ((p >> bb) & 1u) out[o + u++] = e + S * (bb - b0);
-            }
-            carry_pat = __shfl_sync(0xffffffffu, is_idx, 31);
-            dpos += tot;
-        }
-        q += 32 * B;
+    // this warp's segment of the overlapK_w entries, and the role of its first entry: the
+    // parity of its distance to the start of its run (after the last negative entry, or
+    // the block start)
+    const int per = (nin - dmid + 7) / 8;
+    const int q0 = min(nin, dmid + warp * per), q1 = min(nin, q0 + per);
+    int run_start = dmid;
+    for (int p = q0; p > dmid;) {
+        const int lo = max(dmid, p - 32);
+        const int i = lo + lane;
+        const int e = (i < p) ? __ldg(in + Q + i) : 0;
+        const unsigned neg = __ballot_sync(0xffffffffu, i < p && e < 0);
+        if (neg) { run_start = lo + (31 - __clz(neg)) + 1; break; }
+        p = lo;
     }
+    const bool carry = ((q0 - run_start) & 1) != 0;
+    const int cnt = (q0 < q1) ? cps_segment<false>(in, Q, q0, q1, nin, carry, g.S, out, 0) : 0;
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    int base = dmid;
+    for (int w = 0; w < warp; w++) base += s_cnt[w];
+    if (q0 < q1) cps_segment<true>(in, Q, q0, q1, nin, carry, g.S, out, Z + base);
 }
 
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st) {
-    const int wpb = 8;
-    long long blocks = (g.NC + wpb - 1) / wpb;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)blocks);
-    cfg.blockDim = dim3(wpb * 32);
+    cfg.gridDim = dim3((unsigned)g.NC);     // one CTA (8 warp segments) per channel
+    cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
