@@ -9,6 +9,8 @@ c = workload(wl); d = c["desc"]
 if len(sys.argv) > 2:
     d = dict(d, N=int(sys.argv[2]))
 dens = c["density"] if c["density"] is not None else 0.5
+if os.environ.get("PROF_DENSITY"):
+    dens = float(os.environ["PROF_DENSITY"])
 x = clustered_relu(d["N"], d["C"], d["H"], d["W"], dens, c["seed"], c["dead_frac"], c["zero_tile_frac"])
 w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
 L = SparseConvLayer(d, torch.from_numpy(w).cuda())
