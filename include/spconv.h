@@ -141,6 +141,11 @@ spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, 
  * tcgen05 engine.  ws_bytes must be >= 4 * S_im2col. */
 spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const float *w_kcrs, float *y,
                                int32_t fuse_relu, void *ws_lowered, size_t ws_bytes, void *stream);
+/* Recommended ws_bytes for im2col_conv_forward under the current engine: the lowered matrix
+ * (4 * S_im2col, 256-byte aligned) plus, for the tcgen05 engine, 8 * K*C*R*S bytes where the
+ * weights are split once per call into tf32 hi / lo halves (with only 4 * S_im2col the split
+ * happens per tile in shared memory: same results, slower).  Host only. */
+size_t spc_im2col_ws_bytes(const spc_conv_desc *d);
 
 /* GEMM engines of the dense baseline.  im2col_conv_forward uses the process-wide
  * default (spc_set_im2col_gemm; initially SPC_GEMM_AUTO: the tcgen05 3xTF32 kernel for

@@ -77,13 +77,15 @@ _lib.spc_get_im2col_gemm.argtypes = []
 _lib.spc_get_im2col_gemm.restype = ctypes.c_int
 _lib.spc_im2col_engine.argtypes = [ctypes.c_void_p]
 _lib.spc_im2col_engine.restype = ctypes.c_int
+_lib.spc_im2col_ws_bytes.argtypes = [ctypes.c_void_p]
+_lib.spc_im2col_ws_bytes.restype = ctypes.c_size_t
 _lib.spc_select_ws_bytes.argtypes = [_D]
 _lib.spc_select_ws_bytes.restype = _sz
 _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
 EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
-                          "spc_get_im2col_gemm", "spc_im2col_engine"]
+                          "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes"]
 SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
 SPC_GEMM_AUTO = 5
 GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
@@ -101,6 +103,16 @@ def spc_set_im2col_gemm(gemm: int) -> None:
 
 def spc_get_im2col_gemm() -> int:
     return int(_lib.spc_get_im2col_gemm())
+
+
+def spc_im2col_ws_bytes(d: dict) -> int:
+    """Recommended im2col workspace bytes for layer d under the current GEMM engine."""
+    return int(_lib.spc_im2col_ws_bytes(ctypes.byref(make_desc(d))))
+
+
+def alloc_im2col_workspace(d: dict, device="cuda") -> torch.Tensor:
+    """fp32 workspace of spc_im2col_ws_bytes(d) bytes (lowered matrix + split weights)."""
+    return torch.empty((spc_im2col_ws_bytes(d) + 3) // 4, dtype=torch.float32, device=device)
 
 
 def spc_im2col_engine(d: dict) -> int:

@@ -190,7 +190,9 @@ spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const flo
     float* L = static_cast<float*>(ws_lowered);
     spc_status r = cuda_status(spc::launch_im2col(g, x, L, st), "im2col");
     if (r != SPC_OK) return r;
-    const cudaError_t ge = spc::launch_gemm(g, w_kcrs, L, y, fuse_relu, st);
+    const size_t lowered = spc::align_up(need, 256);
+    float* extra = ws_bytes > lowered ? reinterpret_cast<float*>(static_cast<unsigned char*>(ws_lowered) + lowered) : nullptr;
+    const cudaError_t ge = spc::launch_gemm(g, w_kcrs, L, y, fuse_relu, st, extra, extra ? ws_bytes - lowered : 0);
     if (ge == cudaErrorNotSupported)
         return fail(SPC_EUNSUPPORTED, "GEMM engine %d is not supported by the loaded cuBLAS", spc::gemm_engine());
     return cuda_status(ge, "gemm");
@@ -203,6 +205,14 @@ spc_status spc_set_im2col_gemm(spc_gemm gemm) {
 }
 
 spc_gemm spc_get_im2col_gemm(void) { return (spc_gemm)spc::gemm_engine(); }
+
+size_t spc_im2col_ws_bytes(const spc_conv_desc* d) {
+    if (!d || check_desc(d) != SPC_OK) return 0;
+    const spc::Geom g = spc::make_geom(*d);
+    const size_t lowered = spc::align_up((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow, 256);
+    const bool tc = spc::gemm_engine_for(g) == SPC_GEMM_TC_3XTF32;
+    return lowered + (tc ? spc::align_up((size_t)8 * g.K * g.C * g.R * g.S, 256) : 0);
+}
 
 spc_gemm spc_im2col_engine(const spc_conv_desc* d) {
     if (!d || check_desc(d) != SPC_OK) return spc_get_im2col_gemm();
@@ -227,7 +237,7 @@ size_t spc_select_ws_bytes(const spc_conv_desc* d) {
     if (check_desc(d) != SPC_OK) return 0;
     spc::Geom g = spc::make_geom(*d);
     size_t total = 0;
-    const size_t lowered = spc::align_up((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow, 256);
+    const size_t lowered = spc_im2col_ws_bytes(d);
     const size_t yb = spc::align_up((size_t)4 * g.N * g.K * g.Oh * g.Ow, 256);
     const size_t wpb = spc::align_up((size_t)4 * g.K * g.C * g.R * g.S, 256);
     total += lowered + yb + wpb;
@@ -254,13 +264,13 @@ spc_status select_layer_algo(const spc_conv_desc* d, const float* samples, int32
     cudaStream_t st = (cudaStream_t)stream;
     unsigned char* p = static_cast<unsigned char*>(ws);
     auto take = [&](size_t b) { unsigned char* r = p; p += spc::align_up(b, 256); return r; };
-    float* lowered = reinterpret_cast<float*>(take((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow));
+    const size_t lowered_bytes = spc_im2col_ws_bytes(d);
+    float* lowered = reinterpret_cast<float*>(take(lowered_bytes));
     float* y = reinterpret_cast<float*>(take((size_t)4 * g.N * g.K * g.Oh * g.Ow));
     float* wp = reinterpret_cast<float*>(take((size_t)4 * g.K * g.C * g.R * g.S));
     const bool sparse_ok = check_sparse_geometry(d) == SPC_OK;
     g_err.clear();
     const size_t per_sample = (size_t)g.N * g.C * g.H * g.W;
-    const size_t lowered_bytes = (size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow;
     cudaEvent_t e0, e1;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
         return fail(SPC_ECUDA, "event create");

@@ -199,8 +199,10 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
                                cudaStream_t st);
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
-cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
-cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st);
+cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
+                        float* extra = nullptr, size_t extra_bytes = 0);   // extra: workspace beyond the lowered matrix
+cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
+                           float* bsplit);   // bsplit: 2*K*C*R*S floats or null
 int gemm_engine();
 int gemm_engine_for(const Geom& g);   // effective engine of a layer (AUTO / fallbacks resolved)
 void set_gemm_engine(int e);

@@ -292,10 +292,12 @@ static cudaError_t cublas_gemm(const Geom& g, const float* w, const float* L, fl
     return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st) {
+cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
+                        float* extra, size_t extra_bytes) {
     const int eng = effective_engine(g);
     if (eng == SPC_GEMM_TC_3XTF32) {
-        if (tc_layout(g)) return launch_tc_gemm(g, w, L, y, relu, st);
+        const size_t need = (size_t)8 * g.K * g.C * g.R * g.S;   // pre-split weights (hi, lo)
+        if (tc_layout(g)) return launch_tc_gemm(g, w, L, y, relu, st, extra_bytes >= need ? extra : nullptr);
         return cublas_gemm(g, w, L, y, relu, st, SPC_GEMM_CUBLAS_FP32);
     }
     if (eng != SPC_GEMM_SIMT) return cublas_gemm(g, w, L, y, relu, st, eng);

@@ -8,8 +8,10 @@
 //     im2col_t_kernel; B is the caller's KCRS weight tensor, already K-major;
 //   * TMA (2D tensor maps, box = 32 CRS (128 B) x rows, 128-byte swizzle) lands a stage's
 //     K slice in the UMMA K-major SWIZZLE_128B layout (one TMA per operand per stage);
-//   * every fp32 operand x is split in shared memory into hi = x with the 13 low mantissa
-//     bits cleared (exactly representable in tf32) and lo = x - hi (exact):
+//   * every fp32 operand x is split into hi = x with the 13 low mantissa
+//     bits cleared (exactly representable in tf32) and lo = x - hi (exact) -- A in shared
+//     memory by the split warps, B (the weights) once per call into the workspace tail when
+//     the caller provides it (split_b_kernel), else in shared memory too:
 //     D += Ahi*Bhi + Ahi*Blo + Alo*Bhi; the dropped Alo*Blo is ~2^-22 relative -- inside
 //     the 1e-4 fp32 tolerance of north_star, unlike a single TF32 product;
 //   * warp-specialised pipeline over NST stages (mbarriers): warp 0 issues the TMA loads,
@@ -72,9 +74,10 @@ __device__ __forceinline__ void split4(float4& v, float4& lo) {
     v = h;
 }
 
-template <int BN, int NST>
+template <int BN, int NST, bool BPRE>   // BPRE: B arrives pre-split (hi, lo tensor maps)
 __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                               const __grid_constant__ CUtensorMap mapB,
+                                                              const __grid_constant__ CUtensorMap mapBlo,
                                                               int P, int K, int CRS, long long M,
                                                               float* __restrict__ y, int relu) {
     constexpr int A_BYTES = TM * TBK * 4;            // one of raw/hi, lo
@@ -114,6 +117,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+        if (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBlo) : "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -127,9 +131,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                 const int s = kb % NST;
                 if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
                 unsigned char* st = smem + s * STAGE;
-                mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
                 tma_load_2d(st, &mapA, kb * TBK, (int)m0, &full[s]);
                 tma_load_2d(st + 2 * A_BYTES, &mapB, kb * TBK, n0, &full[s]);
+                if (BPRE) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mapBlo, kb * TBK, n0, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                 alo[i] = lo;
             }
 #pragma unroll
-            for (int i = ct; i < B_BYTES / 16; i += NCONV) {
+            for (int i = ct; i < (BPRE ? 0 : B_BYTES / 16); i += NCONV) {
                 float4 v = bb[i], lo;
                 split4(v, lo);
                 bb[i] = v;
@@ -270,22 +275,48 @@ bool make_map(CUtensorMap* map, const float* base, long long rows, int cols, int
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// hi = x with the 13 low mantissa bits cleared, lo = x - hi, over the K x CRS weights (once
+// per call, so the GEMM's split warps only split A)
+__global__ void __launch_bounds__(256) split_b_kernel(const float* __restrict__ w, float* __restrict__ hi,
+                                                      float* __restrict__ lo, long long n) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+        const float v = w[i];
+        const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        hi[i] = h;
+        lo[i] = v - h;
+    }
+}
+
 template <int BN, int NST>
-cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float* W, float* y, int relu,
-                   cudaStream_t st) {
+cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float* W, float* bsplit, float* y,
+                   int relu, cudaStream_t st) {
     constexpr int STAGE = 2 * TM * TBK * 4 + 2 * BN * TBK * 4;
     const size_t smem = (size_t)NST * STAGE + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr[2] = {false, false};
+    const bool pre = bsplit != nullptr;
+    if (!attr[pre]) {
+        cudaError_t e = cudaFuncSetAttribute(pre ? tc_gemm_kernel<BN, NST, true> : tc_gemm_kernel<BN, NST, false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[pre] = true;
     }
     const long long M = (long long)nimg * P;
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, A, M, CRS, TM) || !make_map(&mb, W, K, CRS, BN)) return cudaErrorNotSupported;
+    CUtensorMap ma, mb, mblo;
+    if (!make_map(&ma, A, M, CRS, TM)) return cudaErrorNotSupported;
+    if (pre) {
+        const long long n = (long long)K * CRS;
+        float *hi = bsplit, *lo = bsplit + n;
+        split_b_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(W, hi, lo, n);
+        if (!make_map(&mb, hi, K, CRS, BN) || !make_map(&mblo, lo, K, CRS, BN)) return cudaErrorNotSupported;
+    } else {
+        if (!make_map(&mb, W, K, CRS, BN)) return cudaErrorNotSupported;
+        mblo = mb;
+    }
     dim3 grid((unsigned)((M + TM - 1) / TM), (K + BN - 1) / BN, 1);
-    tc_gemm_kernel<BN, NST><<<grid, TTHREADS, smem, st>>>(ma, mb, P, K, CRS, M, y, relu);
+    if (pre)
+        tc_gemm_kernel<BN, NST, true><<<grid, TTHREADS, smem, st>>>(ma, mb, mblo, P, K, CRS, M, y, relu);
+    else
+        tc_gemm_kernel<BN, NST, false><<<grid, TTHREADS, smem, st>>>(ma, mb, mblo, P, K, CRS, M, y, relu);
     return cudaGetLastError();
 }
 
@@ -299,13 +330,15 @@ bool tc_gemm_supported(const Geom& g, const float* w) {
 
 // y[n] (K x P) = W (K x CRS) * L[n] (CRS x P), fp32 via 3xTF32 on tcgen05; A = the lowered
 // matrix in the K-major layout [N*P][CRS] (im2col_t_kernel).
-cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* A, float* y, int relu, cudaStream_t st) {
+cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* A, float* y, int relu, cudaStream_t st,
+                           float* bsplit) {
     const int P = g.Oh * g.Ow, K = g.K, CRS = g.C * g.R * g.S;
     if (!tc_gemm_supported(g, w) || (reinterpret_cast<uintptr_t>(A) & 15)) return cudaErrorNotSupported;
+    if (reinterpret_cast<uintptr_t>(bsplit) & 15) bsplit = nullptr;
     // N tile: 128 unless the grid would leave SMs idle with it
     const long long mt = ((long long)g.N * P + TM - 1) / TM;
-    if (K <= 64 || mt * ((K + 127) / 128) < 148) return run_tc<64, 4>(P, K, CRS, g.N, A, w, y, relu, st);
-    return run_tc<128, 3>(P, K, CRS, g.N, A, w, y, relu, st);
+    if (K <= 64 || mt * ((K + 127) / 128) < 148) return run_tc<64, 4>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
+    return run_tc<128, 3>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
 }
 
 }  // namespace spc

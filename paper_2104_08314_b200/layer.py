@@ -38,9 +38,8 @@ class SparseConvLayer:
     @property
     def lowered(self) -> torch.Tensor:
         if self._lowered is None:
-            d = self.d
-            self._lowered = torch.empty(d["N"] * d["C"] * d["R"] * d["S"] * self.Oh * self.Ow,
-                                        dtype=torch.float32, device=self.device)
+            # lowered matrix + (tcgen05 engine) the once-per-call split of the weights
+            self._lowered = B.alloc_im2col_workspace(self.d, device=self.device)
         return self._lowered
 
     # -- the three algorithms (asynchronous on the current stream)

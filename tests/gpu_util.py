@@ -42,7 +42,7 @@ class GpuLayer:
     def im2col(self, x: torch.Tensor, relu: bool = False) -> torch.Tensor:
         Oh, Ow = spc.out_hw(self.d)
         d = self.d
-        L = torch.empty(d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow, dtype=torch.float32, device="cuda")
+        L = spc.alloc_im2col_workspace(d)
         y = torch.empty_like(self.y)
         spc.im2col_conv_forward(d, x, self.w, y, relu, L)
         return y

@@ -350,6 +350,26 @@ def test_im2col_gemm_engines_within_tolerance(oracle_mod, engine):
         spc.spc_set_im2col_gemm(prev)
 
 
+def test_tc_gemm_minimal_workspace(oracle_mod):
+    """With only the lowered matrix as workspace (4 * S_im2col) the tcgen05 engine splits the
+    weights per tile in shared memory instead of once into the workspace tail: same tolerance."""
+    d = layer_desc(2, 256, 14, 14, 256, 3, 3, 1, 1, 1, 1, 1, 1)
+    x = clustered_relu(2, 256, 14, 14, 0.3, 13)
+    w = he_normal(256, 256, 3, 3, 13)
+    ref = oracle_mod.direct_conv(d, x, w)
+    prev = spc.spc_get_im2col_gemm()
+    try:
+        spc.spc_set_im2col_gemm(spc.SPC_GEMM_TC_3XTF32)
+        Oh, Ow = spc.out_hw(d)
+        ws = torch.empty(2 * 256 * 9 * Oh * Ow, dtype=torch.float32, device="cuda")
+        assert 4 * ws.numel() < spc.spc_im2col_ws_bytes(d)
+        y = torch.empty((2, 256, Oh, Ow), dtype=torch.float32, device="cuda")
+        spc.im2col_conv_forward(d, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), y, False, ws)
+        _check_conv(y.cpu().numpy(), ref, "tc 3xtf32, minimal workspace")
+    finally:
+        spc.spc_set_im2col_gemm(prev)
+
+
 def test_im2col_tf32_engine_runs():
     """The 1-term TF32 engine is a crossover reference only: it must run, not meet 1e-4."""
     d = layer_desc(1, 16, 14, 14, 16, 3, 3, 1, 1, 1, 1, 1, 1)
