@@ -94,10 +94,14 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
     __shared__ __align__(8) unsigned long long full[NST], conv[NST], empty[NST], accf[2], acce[2];
     __shared__ unsigned tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long m0 = (long long)blockIdx.x * TM;
-    const int n0 = blockIdx.y * BN;
+    // persistent: CTA b takes tiles b, b + gridDim.x, ... (tile = n-tile major over m-tiles);
+    // the stage ring and the two TMEM chunk buffers run on across tiles (flat counters)
+    const long long mtiles = (M + TM - 1) / TM;
+    const long long ntile_total = mtiles * ((K + BN - 1) / BN);
     const int nk = (CRS + TBK - 1) / TBK;
-    const int nch = (nk + KCH - 1) / KCH;           // accumulation chunks
+    const int nch = (nk + KCH - 1) / KCH;           // accumulation chunks per tile
+    auto tile_m0 = [&](long long t) { return (t % mtiles) * TM; };
+    auto tile_n0 = [&](long long t) { return (int)(t / mtiles) * BN; };
 
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -127,14 +131,18 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (warp == 0) {
         // ---- TMA producer: raw A (rows m0..) and B (output channels n0..) tiles of a stage
         if (lane == 0) {
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % NST;
-                if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
-                unsigned char* st = smem + s * STAGE;
-                mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
-                tma_load_2d(st, &mapA, kb * TBK, (int)m0, &full[s]);
-                tma_load_2d(st + 2 * A_BYTES, &mapB, kb * TBK, n0, &full[s]);
-                if (BPRE) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mapBlo, kb * TBK, n0, &full[s]);
+            long long g = 0;   // stage counter across tiles
+            for (long long t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+                const int m0 = (int)tile_m0(t), n0 = tile_n0(t);
+                for (int kb = 0; kb < nk; kb++, g++) {
+                    const int s = (int)(g % NST);
+                    if (g >= NST) mbar_wait(&empty[s], (unsigned)(((g / NST) - 1) & 1));
+                    unsigned char* st = smem + s * STAGE;
+                    mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
+                    tma_load_2d(st, &mapA, kb * TBK, m0, &full[s]);
+                    tma_load_2d(st + 2 * A_BYTES, &mapB, kb * TBK, n0, &full[s]);
+                    if (BPRE) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mapBlo, kb * TBK, n0, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -143,11 +151,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
         //      committed to accf[j & 1] for the drain warps
         if (lane == 0) {
             const unsigned sbase = smem_u32(smem);
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % NST, j = kb / KCH, b = j & 1;
+            long long g = 0, jg = 0;   // stage and chunk counters across tiles
+            for (long long t = blockIdx.x; t < ntile_total; t += gridDim.x)
+            for (int kb = 0; kb < nk; kb++, g++) {
+                const int s = (int)(g % NST), b = (int)(jg & 1);
                 const bool first = (kb % KCH) == 0, last = (kb % KCH) == KCH - 1 || kb == nk - 1;
-                if (first && j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);
-                mbar_wait(&conv[s], (kb / NST) & 1);
+                if (first && jg >= 2) mbar_wait(&acce[b], (unsigned)(((jg >> 1) - 1) & 1));
+                mbar_wait(&conv[s], (unsigned)((g / NST) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const unsigned sa = sbase + s * STAGE;
                 const unsigned dt = tmem + (unsigned)(b * BN);
@@ -169,17 +179,20 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                              ::"r"(smem_u32(&empty[s])) : "memory");
-                if (last)
+                if (last) {
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                                  ::"r"(smem_u32(&accf[b])) : "memory");
+                    jg++;
+                }
             }
         }
     } else if (warp < 2 + NCONV / 32) {
         // ---- converter warps: split every landed stage into hi (in place) and lo
         const int ct = tid - 64;
-        for (int kb = 0; kb < nk; kb++) {
-            const int s = kb % NST;
-            mbar_wait(&full[s], (kb / NST) & 1);
+        const long long gtot = ((ntile_total - blockIdx.x + gridDim.x - 1) / gridDim.x) * nk;
+        for (long long g = 0; g < gtot; g++) {
+            const int s = (int)(g % NST);
+            mbar_wait(&full[s], (unsigned)((g / NST) & 1));
             unsigned char* st = smem + s * STAGE;
             float4* a = reinterpret_cast<float4*>(st);
             float4* alo = reinterpret_cast<float4*>(st + A_BYTES);
@@ -208,12 +221,16 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
         //      then store y; two warps per TMEM lane quarter, half the columns each
         const int dw = warp - 2 - NCONV / 32;          // 0..7
         const int q = warp & 3, half = dw >> 2;        // a warp may access TMEM lanes 32 (warp % 4) ..
+        long long jg = 0;
+        for (long long t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+        const long long m0 = tile_m0(t);
+        const int n0 = tile_n0(t);
         float sum[HALF];
 #pragma unroll
         for (int i = 0; i < HALF; i++) sum[i] = 0.f;
-        for (int j = 0; j < nch; j++) {
-            const int b = j & 1;
-            mbar_wait(&accf[b], (j >> 1) & 1);
+        for (int j = 0; j < nch; j++, jg++) {
+            const int b = (int)(jg & 1);
+            mbar_wait(&accf[b], (unsigned)((jg >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int c0 = 0; c0 < HALF; c0 += 16) {
@@ -241,11 +258,22 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                 if (kout < K) yrow[(size_t)kout * P] = relu ? fmaxf(sum[i], 0.f) : sum[i];
             }
         }
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((unsigned)(2 * BN)) : "memory");
+}
+
+int sm_count_tc() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+    }
+    return n;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -312,7 +340,9 @@ cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float*
         if (!make_map(&mb, W, K, CRS, BN)) return cudaErrorNotSupported;
         mblo = mb;
     }
-    dim3 grid((unsigned)((M + TM - 1) / TM), (K + BN - 1) / BN, 1);
+    // persistent grid: one CTA per SM (the kernel's shared memory allows one)
+    const long long tiles = ((M + TM - 1) / TM) * ((K + BN - 1) / BN);
+    dim3 grid((unsigned)std::min<long long>(tiles, sm_count_tc()), 1, 1);
     if (pre)
         tc_gemm_kernel<BN, NST, true><<<grid, TTHREADS, smem, st>>>(ma, mb, mblo, P, K, CRS, M, y, relu);
     else
