@@ -4,6 +4,7 @@
 // (SI Eq. 6 elements per image), written coalesced along the output position.
 // GEMM: y[n] (K x P) = W (K x CRS) * L[n] (CRS x P), P = Oh*Ow, FP32.
 #include <algorithm>
+#include <cstdlib>
 #include <cublas_v2.h>
 #include <mutex>
 
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(256) im2col_row_kernel(Geom g, const float* __
 // divisions) into a column-major smem tile, then write each position's C*R*S slice with
 // lanes along CRS (coalesced 128-byte rows).  The tile is [CB*R*S][33] so both phases are
 // bank-conflict free.
-constexpr int kTcCB = 32;
+constexpr int kTcCB = 64;
 template <int R_, int S_>   // compile-time taps (all loads of a channel in flight), or 0, 0: runtime
 __global__ void __launch_bounds__(256) im2col_t_kernel(Geom g, const float* __restrict__ x, float* __restrict__ A,
                                                        int cb) {
@@ -129,7 +130,10 @@ cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t 
     if (tc_layout(g)) {
         const long long M = (long long)g.N * g.Oh * g.Ow;
         const int RS = g.R * g.S;
-        const int cb = std::max(1, std::min(kTcCB, 320 / RS));     // tile <= 320 x 33 floats (42 KB)
+        // channels per block: longer contiguous row segments per position write faster
+        // (batch-256 cfg5-L0: 32 -> 496 us, 64 -> 467 us; 128 is slower: 1 block/SM)
+        // (larger taps: 5x5 @35 is faster with 12 channels, 42 KB, than with 25, 82 KB)
+        const int cb = (RS <= 9) ? std::min(kTcCB, 640 / RS) : std::max(1, std::min(32, 320 / RS));
         const size_t smem = (size_t)cb * RS * 33 * sizeof(float);
         auto kern = (g.R == 3 && g.S == 3) ? im2col_t_kernel<3, 3>
                   : (g.R == 1 && g.S == 7) ? im2col_t_kernel<1, 7>
