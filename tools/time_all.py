@@ -43,6 +43,8 @@ def main():
         if os.environ.get("TIME_BATCH"):          # e.g. 256: the stack's per-GPU batch at N=1
             d = dict(d, N=int(os.environ["TIME_BATCH"]))
         dens = c["density"] if c["density"] is not None else 0.5
+        if os.environ.get("TIME_DENSITY"):
+            dens = float(os.environ["TIME_DENSITY"])
         x = clustered_relu(d["N"], d["C"], d["H"], d["W"], dens, c["seed"], c["dead_frac"], c["zero_tile_frac"])
         w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
         xg, wg = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
