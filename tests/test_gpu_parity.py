@@ -184,6 +184,10 @@ def test_balanced_mode_full(oracle_mod, shape, capfd, monkeypatch):
     for _ in range(3):
         assert np.array_equal(L.conv().cpu().numpy(), y1)
     _check_conv(L.conv(relu=True).cpu().numpy(), np.maximum(ref, 0.0), "balanced mode + relu")
+    # CPS: the expanded indices feed the same balanced conv
+    L.encode(torch.from_numpy(x).cuda(), cps=True)
+    assert_streams_equal(L.streams(), oracle_mod.encode(d, x, cps=True), "balanced cps")
+    _check_conv(L.conv().cpu().numpy(), ref, "balanced mode, CPS")
 
 
 def _stream_slice(enc_gpu, c0, c1):
