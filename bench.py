@@ -69,6 +69,17 @@ def nze_macs(d, x: np.ndarray, Oh, Ow) -> int:
     return int(ch @ nz @ cw) * d["K"]
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def tf32_peak():
     """Dense TF32 tensor peak, TFLOP/s: the measured bf16 peak (MEASURED_PEAKS.json) times the
     guide's nominal tf32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)."""
@@ -328,18 +339,24 @@ def run_ours(args):
     g_i2c = L_cpo.capture(lambda: L_cpo.forward(xg, "im2col"))
     L_cpo.forward(xg, "cpo")       # leave the CPO encoding in place for the conv-only graph
 
-    def timed(graph, steps, warmup):
+    step_ms = {}
+
+    def timed(graph, steps, warmup, flush_l2=True, key=None):
         for _ in range(warmup):
             graph.replay()
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         for i in range(steps):
-            flush.zero_()                      # L2 flush between timed steps (outside the events)
+            if flush_l2:
+                flush.zero_()                  # L2 flush between timed steps (outside the events)
             ev[i][0].record(stream)
             graph.replay()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-        return sum(a.elapsed_time(b) for a, b in ev)
+        ts = [a.elapsed_time(b) for a, b in ev]
+        if key:
+            step_ms[key] = ts
+        return sum(ts)
 
     # --- main timed region (CPO path), barrier + sync on both sides, max over ranks
     for _ in range(args.warmup):
@@ -348,7 +365,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        t_ms = timed(g_cpo, args.steps, 0)
+        t_ms = timed(g_cpo, args.steps, 0, key="cpo")
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -361,6 +378,7 @@ def run_ours(args):
     value = flops_step * args.steps * world / (tmax * 1e-3) / 1e9
 
     # --- per-kernel breakdown and the other algorithms (same process)
+    t_hot_ms = timed(g_cpo, args.steps, 1, flush_l2=False)   # hot L2: no flush
     t_enc_ms = timed(g_cpo_enc, args.steps, 1)
     t_conv_ms = timed(g_cpo_conv, args.steps, 1)
     t_cps = timed(g_cps, args.steps, 1)
@@ -429,6 +447,7 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu:
         t, n, f = oracle_time(d, x, w, budget_s=args.cpu_budget)
         cpu = {"value": f / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+               "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
                "sample": f"{n} image(s) of {args.workload}: oracle CPO encode + Alg. 2 conv, single thread, FP64"}
 
     stack = None
@@ -443,11 +462,13 @@ def run_ours(args):
             "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step_median": float(np.median(step_ms["cpo"])) if rank == 0 else None,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"],
                        "dead_frac": c["dead_frac"], "zero_tile_frac": c["zero_tile_frac"],
                        "l2": "flushed between timed steps (256 MiB write)", "global_batch": d["N"] * world},
             "layer_us": {"cpo_encode": us(t_enc_ms), "cpo_conv": us(t_conv_ms), "cpo_total": us(t_ms),
+                         "cpo_total_hot_l2": us(t_hot_ms),
                          "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
                          "im2col_total": us(t_i2c)},
             "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
