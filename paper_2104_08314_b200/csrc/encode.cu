@@ -628,16 +628,24 @@ int sm_count() {
     return n;
 }
 
-// Tile size: about one tile per resident CTA (2 per SM when the tile fits in
-// ~100 KB of smem, else 1), capped by the shared-memory stage.
+// Tile size: prefer 2 resident CTAs per SM (tiles within ~110 KB of smem), else 1; take
+// the fewest rounds that largest tile allows, then the smallest P that still needs only
+// that many rounds, so every round is (nearly) full.  Measured: cfg5-L7 (batch 32) 71 -> 50 us
+// (a 51-plane tile at 1 CTA/SM had left a 13-tile second round), batch 256 L4 176 -> 147 us,
+// L14 137 -> 102 us; one-round launches are unchanged (cfg2: P = 1, cfg5-L0: P = 7).
 EncPlan plan_encode(const Geom& g) {
     EncPlan pl;
     const int sms = sm_count();
     const size_t b2 = 110 * 1024, b1 = 220 * 1024;
-    long long P = (g.NC + 2 * sms - 1) / (2 * sms);
-    if (enc_smem_layout(g, (int)P).total > b2) {
-        P = (g.NC + sms - 1) / sms;
-        while (P > 1 && enc_smem_layout(g, (int)P).total > b1) P--;
+    long long P = 0;
+    for (int per_sm = 2; per_sm >= 1 && P == 0; per_sm--) {
+        const size_t budget = (per_sm == 2) ? b2 : b1;
+        long long pmax = 0;
+        while (pmax < g.NC && enc_smem_layout(g, (int)(pmax + 1)).total <= budget) pmax++;
+        if (pmax == 0) continue;
+        const long long slots = (long long)per_sm * sms;
+        const long long rounds = (g.NC + slots * pmax - 1) / (slots * pmax);
+        P = (g.NC + slots * rounds - 1) / (slots * rounds);
     }
     pl.P = (int)std::max(1ll, P);
     pl.ntiles = (int)((g.NC + pl.P - 1) / pl.P);
