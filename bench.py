@@ -385,6 +385,34 @@ def run_ours(args):
     t_cps_enc = timed(g_cps_enc, args.steps, 1)
     t_i2c = timed(g_i2c, args.steps, 1)
 
+    # Per-launch kernel durations for the rooflines: timing events recorded INSIDE a
+    # graph right around the one kernel (external event-record nodes on the stream
+    # the kernel is launched on), an L2 flush before each, so the graph launch and
+    # the event round trip to the host (~6 us per step on this pool) are not in it.
+    def kernel_timed(fn, steps, reps=50):
+        reps = max(1, min(reps, steps))
+        evs = [(torch.cuda.Event(enable_timing=True, external=True),
+                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(reps)]
+
+        def body():
+            for a, b in evs:
+                flush.zero_()
+                a.record()
+                fn()
+                b.record()
+        g = L_cpo.capture(body, warmup=1)
+        ts = []
+        for _ in range(max(1, steps // reps) + 1):   # first replay is warm-up
+            g.replay()
+            torch.cuda.synchronize()
+            ts.append([a.elapsed_time(b) for a, b in evs])
+        ts = [t for row in ts[1:] for t in row]
+        return float(np.mean(ts)), float(np.median(ts))
+
+    k_conv_ms, k_conv_med = kernel_timed(lambda: L_cpo.conv(), args.steps)
+    k_enc_ms, k_enc_med = kernel_timed(lambda: L_cpo.encode(xg, "cpo"), args.steps)
+    L_cpo.forward(xg, "cpo")
+
     # encoding sizes, CR (paper units: elements of ptr + DA + IN vs S_im2col)
     pl_, dl_, il_ = spc.spc_encoding_lengths(enc)
     ps_, ds_, is_ = spc.spc_encoding_lengths(enc_s)
@@ -399,8 +427,8 @@ def run_ours(args):
     macs = nze_macs(d, x, Oh, Ow)
     conv_bytes = 4 * (pl_ + dl_ + il_) + 8 * 2 * (d["N"] * d["C"] + 1) + 4 * wg.numel() + 4 * y.numel()
     enc_bytes = 4 * xg.numel() + 4 * (pl_ + dl_ + il_) + 8 * 3 * (d["N"] * d["C"] + 1)
-    conv_s = t_conv_ms / args.steps * 1e-3
-    enc_s = t_enc_ms / args.steps * 1e-3
+    conv_s = k_conv_ms * 1e-3          # average launch duration (in-graph events)
+    enc_s = k_enc_ms * 1e-3
     conv_flops = 2.0 * macs
     t_roof_conv = max(conv_bytes / (hbm_gbs * 1e9), conv_flops / (p_fp32 * 1e12))
     conv_bound = "alu" if conv_flops / (p_fp32 * 1e12) >= conv_bytes / (hbm_gbs * 1e9) else "hbm"
@@ -416,7 +444,8 @@ def run_ours(args):
             roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "alu", "achieved": conv_flops / conv_s / 1e12,
                     "peak": p_fp32, "unit": "TFLOP/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
                     "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
-                    "algorithmic_flops": conv_flops, "algorithmic_bytes": conv_bytes}
+                    "algorithmic_flops": conv_flops, "algorithmic_bytes": conv_bytes,
+                    "duration_us": conv_s * 1e6}
         else:
             roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "hbm", "achieved": conv_bytes / conv_s / 1e9,
                     "peak": hbm_gbs, "unit": "GB/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
@@ -471,6 +500,9 @@ def run_ours(args):
                          "cpo_total_hot_l2": us(t_hot_ms),
                          "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
                          "im2col_total": us(t_i2c)},
+            "kernel_us": {"timing": "per launch, timing events inside a graph around the one kernel, L2 flushed before each",
+                          "cpo_conv_mean": 1e3 * k_conv_ms, "cpo_conv_median": 1e3 * k_conv_med,
+                          "cpo_encode_mean": 1e3 * k_enc_ms, "cpo_encode_median": 1e3 * k_enc_med},
             "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
                        "gemm": spc.GEMM_NAMES[spc.spc_im2col_engine(d)]},
             "speedup_vs_im2col": t_i2c / t_ms,
