@@ -15,7 +15,7 @@ if not torch.cuda.is_available():
 
 from gpu_util import GpuLayer, assert_streams_equal  # noqa: E402
 from helpers import within_tol, valid_sparse_geometry  # noqa: E402
-from synth import (CONFIGS, cfg5_layers, clustered_relu, he_normal, int_map, int_weights,  # noqa: E402
+from synth import (CATALOG, CONFIGS, cfg5_layers, clustered_relu, he_normal, int_map, int_weights,  # noqa: E402
                    layer_desc)
 
 import paper_2104_08314_b200 as spc  # noqa: E402
@@ -129,7 +129,7 @@ def test_cfg4_pair_relu_chain(oracle_mod):
     _layer_case(oracle_mod, db, y1, w2, full=True)
 
 
-@pytest.mark.parametrize("li", [0, 3, 4, 8, 12, 15])
+@pytest.mark.parametrize("li", range(16))
 def test_cfg5_layers_sampled(oracle_mod, li):
     layer = cfg5_layers(batch=32)[li]
     d = layer["desc"]
@@ -138,11 +138,10 @@ def test_cfg5_layers_sampled(oracle_mod, li):
     _layer_case(oracle_mod, d, x, w, full=False, samples=3000, seed=li)
 
 
-@pytest.mark.parametrize("name", ["iv3_5x5_35", "iv3_1x3_8", "iv3_7x1_17", "vgg_3x3_112", "s2_3x3_112"])
+@pytest.mark.parametrize("name", sorted(CATALOG))
 def test_catalog_shapes_sampled(oracle_mod, name):
-    """Shape-catalog layers (5x5, 1x3, 7x1 kernels; a 112x112 map on the generic kernel):
+    """Every shape-catalog layer (5x5, 3x3, 1x7, 7x1, 1x3, 3x1 kernels; 112x112 maps at s1 / s2):
     encodings bit-exact, sampled outputs of CPO / CPS / im2col within tolerance."""
-    from synth import CATALOG
     c = CATALOG[name]
     d = c["desc"]
     x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"])
