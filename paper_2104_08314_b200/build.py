@@ -33,15 +33,21 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, probes: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, probes: bool = False, variant: str = "") -> str:
+    """variant: a dev A/B build, `name:-DFOO,-DBAR` -> libspconv_<name>.so (loaded via
+    SPC_LIB_OVERRIDE by the timing tools only)."""
+    vname, vdefs = (variant.split(":", 1) + [""])[:2] if variant else ("", "")
     lib = LIB.replace(".so", "_probe.so") if probes else LIB
-    if not force and not probes and not stale():
+    if vname:
+        lib = LIB.replace(".so", f"_{vname}.so")
+    if not force and not probes and not vname and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    obj_dir = OBJ + ("_probe" if probes else "")
+    obj_dir = OBJ + ("_probe" if probes else "") + (f"_{vname}" if vname else "")
     os.makedirs(obj_dir, exist_ok=True)
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              f"-DSPC_GIT_REV=\"{_git_rev()}\""] + (["-Xptxas=-v"] if verbose else []) + (["-DSPC_PROBES"] if probes else [])
+              f"-DSPC_GIT_REV=\"{_git_rev()}\""] + (["-Xptxas=-v"] if verbose else []) + (["-DSPC_PROBES"] if probes else []) + \
+        [d for d in vdefs.split(",") if d]
 
     def compile_one(src: str) -> str:
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
@@ -56,4 +62,5 @@ def build(force: bool = False, verbose: bool = False, probes: bool = False) -> s
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv, variant=var))
