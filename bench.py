@@ -197,6 +197,26 @@ def oracle_time_threads(d, x, w, budget_s: float, threads: int):
     return t_used, n_done, flops, len(bounds)
 
 
+def oracle_legs(d, x, w):
+    """The oracle's other algorithms on one image, single thread: CPS encode +
+    Alg. 4, the direct nested-loop conv (Eq. 1) and im2col + naive GEMM; dense-equiv. GFLOP/s."""
+    import oracle
+    oracle.build()
+    d1 = dict(d, N=1)
+    Oh, Ow = oracle.out_hw(d1)
+    f = dense_flops(d1, Oh, Ow)
+    xi = x[:1]
+    out = {}
+    for name, fn in (("cps", lambda: oracle.sparse_conv(d1, oracle.encode(d1, xi, cps=True), w)),
+                     ("direct", lambda: oracle.direct_conv(d1, xi, w)),
+                     ("im2col_gemm", lambda: oracle.gemm_lowered(d1, oracle.im2col(d1, xi), w))):
+        t0 = time.perf_counter()
+        fn()
+        out[name] = f / (time.perf_counter() - t0) / 1e9
+    out["unit"] = "GFLOP/s (dense-equivalent, one image, one thread)"
+    return out
+
+
 def run_reference(args):
     """--impl reference: the oracle as the reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -549,6 +569,7 @@ def run_ours(args):
         cpu = {"value": f / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
                "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
                "sample": f"{n} image(s) of {args.workload}: oracle CPO encode + Alg. 2 conv, single thread, FP64"}
+        cpu["legs"] = oracle_legs(d, x, w)
         t2, n2, f2, thr = oracle_time_threads(d, x, w, args.cpu_budget, os.cpu_count() or 1)
         cpu["all_cores"] = {"value": f2 / t2 / 1e9, "unit": "GFLOP/s", "cores": thr,
                             "sample": f"{n2} image(s): encode on one thread, Alg. 2 over {thr} output-channel "
