@@ -947,8 +947,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         if (a.cg == 1) {
             // no cluster split: store straight from registers (a lane owns output channel
             // kk*32+lane and a 4-wide output row per accumulator chunk).  With a cluster split
-            // the DSMEM reduction below wins: measured, red.global.add.v4 of every rank's
-            // partial costs 8x the transactions and is slower at cfg2/cfg3.
+            // the L2 (or, without scratch, DSMEM) reduction below wins: measured,
+            // red.global.add.v4 of every rank's partial costs 8x the transactions and is
+            // slower at cfg2/cfg3.
             auto emit = [&](bool add) {
 #pragma unroll
                 for (int i = 0; i < T::NACC / 4; i++) {
