@@ -142,14 +142,15 @@ spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, 
 spc_status im2col_conv_forward(const spc_conv_desc *d, const float *x, const float *w_kcrs, float *y,
                                int32_t fuse_relu, void *ws_lowered, size_t ws_bytes, void *stream);
 /* Recommended ws_bytes for im2col_conv_forward under the current engine: the lowered matrix
- * (4 * S_im2col, 256-byte aligned) plus, for the tcgen05 engine, 8 * K*C*R*S bytes where the
- * weights are split once per call into tf32 hi / lo halves (with only 4 * S_im2col the split
- * happens per tile in shared memory: same results, slower).  Host only. */
+ * (4 * S_im2col, 256-byte aligned) plus, for the tcgen05 engine, 4 * K*C*R*S bytes where the
+ * weights' lo halves (w minus its tf32 truncation) are formed once per call (with only
+ * 4 * S_im2col they are formed per tile in shared memory: same results, slower).  Host only. */
 size_t spc_im2col_ws_bytes(const spc_conv_desc *d);
 
 /* GEMM engines of the dense baseline.  im2col_conv_forward uses the process-wide
  * default (spc_set_im2col_gemm; initially SPC_GEMM_AUTO: the tcgen05 3xTF32 kernel for
- * layers of >= 2^28 MACs with C*R*S % 4 == 0 (its TMA row pitches), cuBLAS FP32 otherwise,
+ * layers of >= 2^28 MACs, or >= 2^26 MACs over >= 20 output tiles of 128 positions x 64
+ * (K <= 64) or 128 channels, with C*R*S % 4 == 0 (its TMA row pitches), cuBLAS FP32 otherwise,
  * both within the 1e-4 tolerance).  SPC_GEMM_TC_3XTF32 also falls back to cuBLAS FP32
  * when C*R*S % 4 != 0.  An engine the
  * loaded cuBLAS lacks makes im2col_conv_forward return SPC_EUNSUPPORTED (BF16X9

@@ -211,7 +211,7 @@ size_t spc_im2col_ws_bytes(const spc_conv_desc* d) {
     const spc::Geom g = spc::make_geom(*d);
     const size_t lowered = spc::align_up((size_t)4 * g.N * g.C * g.R * g.S * g.Oh * g.Ow, 256);
     const bool tc = spc::gemm_engine_for(g) == SPC_GEMM_TC_3XTF32;
-    return lowered + (tc ? spc::align_up((size_t)8 * g.K * g.C * g.R * g.S, 256) : 0);
+    return lowered + (tc ? spc::align_up((size_t)4 * g.K * g.C * g.R * g.S, 256) : 0);
 }
 
 spc_gemm spc_im2col_engine(const spc_conv_desc* d) {

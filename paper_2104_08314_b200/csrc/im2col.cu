@@ -14,12 +14,18 @@ namespace spc {
 
 static int g_gemm = SPC_GEMM_AUTO;   // im2col GEMM engine (spc_set_im2col_gemm)
 
-// The engine a layer actually runs: AUTO picks the tcgen05 kernel for large layers
-// (measured faster from cfg3 up: 66 vs 98 us; cfg2, 1.2e8 MACs: 31 vs 29 us for cuBLAS).
+// The engine a layer actually runs: AUTO picks the tcgen05 kernel for layers of >= 2^28
+// MACs, or >= 2^26 MACs spread over >= 20 output tiles (128 positions x 64 / 128 channels)
+// -- measured (lowering + GEMM, graph, L2 flushed): cfg2 (1.2e8 MACs, 25 tiles) 26.7 vs
+// 28.7 us for cuBLAS FP32, cfg3 61 vs 98; Inception 1x3 @8 (2.3e8 MACs, 12 tiles) 41 vs 39,
+// cfg1 (4.5e5 MACs) 16 vs 12.
 static int effective_engine(const Geom& g) {
     if (g_gemm != SPC_GEMM_AUTO) return g_gemm;
     const double macs = (double)g.N * g.Oh * g.Ow * g.K * g.C * g.R * g.S;
-    return (macs >= 268435456.0) ? SPC_GEMM_TC_3XTF32 : SPC_GEMM_CUBLAS_FP32;
+    const long long mt = ((long long)g.N * g.Oh * g.Ow + 127) / 128, bn = g.K <= 64 ? 64 : 128;
+    const long long tiles = mt * ((g.K + bn - 1) / bn);
+    return (macs >= 268435456.0 || (macs >= 67108864.0 && tiles >= 20)) ? SPC_GEMM_TC_3XTF32
+                                                                        : SPC_GEMM_CUBLAS_FP32;
 }
 
 // Block (32, 8): threadIdx.x strides 32 consecutive output positions of a lowered row
@@ -300,7 +306,7 @@ cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y,
                         float* extra, size_t extra_bytes) {
     const int eng = effective_engine(g);
     if (eng == SPC_GEMM_TC_3XTF32) {
-        const size_t need = (size_t)8 * g.K * g.C * g.R * g.S;   // pre-split weights (hi, lo)
+        const size_t need = (size_t)4 * g.K * g.C * g.R * g.S;   // the weights' lo half
         if (tc_layout(g)) return launch_tc_gemm(g, w, L, y, relu, st, extra_bytes >= need ? extra : nullptr);
         return cublas_gemm(g, w, L, y, relu, st, SPC_GEMM_CUBLAS_FP32);
     }

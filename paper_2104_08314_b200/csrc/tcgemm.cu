@@ -9,13 +9,17 @@
 //   * TMA (2D tensor maps, box = 32 CRS (128 B) x rows, 128-byte swizzle) lands a stage's
 //     K slice in the UMMA K-major SWIZZLE_128B layout (one TMA per operand per stage);
 //   * every fp32 operand x is split into hi = x with the 13 low mantissa
-//     bits cleared (exactly representable in tf32) and lo = x - hi (exact) -- A in shared
-//     memory by the split warps, B (the weights) once per call into the workspace tail when
-//     the caller provides it (split_b_kernel), else in shared memory too:
+//     bits cleared (exactly representable in tf32) and lo = x - hi (exact); kind::tf32
+//     reads only the top 19 bits of a 32-bit operand, so the raw x is passed as hi and only
+//     lo is materialised -- for A by the split warps, which move each landed A tile (raw =
+//     hi, and lo) from shared memory into TMEM (tcgen05.st; the MMAs take A from TMEM, so
+//     they read only B from shared memory: the ring is shared-memory-bandwidth-bound), for
+//     B (the weights) once per call into the workspace tail when the caller provides it
+//     (split_b_kernel), else in shared memory by the split warps:
 //     D += Ahi*Bhi + Ahi*Blo + Alo*Bhi; the dropped Alo*Blo is ~2^-22 relative -- inside
 //     the 1e-4 fp32 tolerance of north_star, unlike a single TF32 product;
 //   * warp-specialised pipeline over NST stages (mbarriers): warp 0 issues the TMA loads,
-//     warps 2-5 split the landed tiles in place (hi) and into a lo buffer, warp 1 issues
+//     warps 2-5 (thread = A row = TMEM lane) write hi / lo of every landed A tile to TMEM, warp 1 issues
 //     the 12 MMAs of a stage (M = 128, N = BN, K = 8 each) and commits them to the stage's
 //     "empty" barrier;
 //   * accuracy: the tensor core's fp32 accumulation over all of CRS (x3 products) left
@@ -39,6 +43,12 @@ constexpr int NCONV = 128;    // converter threads (warps 2-5)
 constexpr int NDRAIN = 256;   // drain / epilogue threads (warps 6-13)
 constexpr int TTHREADS = 64 + NCONV + NDRAIN;   // + warp 0 TMA, warp 1 MMA
 constexpr int KCH = 8;        // stages (8 x 32 CRS) per TMEM accumulation chunk
+#ifndef SPC_TC_NST64
+#define SPC_TC_NST64 4
+#endif
+#ifndef SPC_TC_NST128
+#define SPC_TC_NST128 4
+#endif
 
 // SmemDescriptor (sm_100) of a K-major operand tile in the 128-byte swizzle layout that TMA
 // writes (rows of 128 B = 32 fp32, 16-byte chunks XOR-ed with row % 8 inside each 1024-byte
@@ -58,36 +68,52 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
 }
 
+// 32 consecutive TMEM columns of this thread's lane (32x32b shape, one register per column)
+__device__ __forceinline__ void tmem_st32(unsigned taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+          "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+          "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// hi = x with the 13 low mantissa bits cleared (a tf32 value), lo = x - hi (exact in fp32)
-__device__ __forceinline__ void split4(float4& v, float4& lo) {
+// lo = x - hi (exact in fp32), hi = x with the 13 low mantissa bits cleared (a tf32 value).
+// hi itself is never written: kind::tf32 reads only the top 19 bits of each 32-bit operand,
+// so the raw x already is hi to the tensor core (measured: outputs bit-identical to staging
+// explicitly truncated copies, and 5-8 % faster on the K >= 128 layers: one smem write pass
+// fewer per stage).
+__device__ __forceinline__ float4 lo_of(const float4 v) {
     const unsigned M = 0xFFFFE000u;
-    float4 h;
-    h.x = __uint_as_float(__float_as_uint(v.x) & M);
-    h.y = __uint_as_float(__float_as_uint(v.y) & M);
-    h.z = __uint_as_float(__float_as_uint(v.z) & M);
-    h.w = __uint_as_float(__float_as_uint(v.w) & M);
-    lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-    v = h;
+    return make_float4(v.x - __uint_as_float(__float_as_uint(v.x) & M), v.y - __uint_as_float(__float_as_uint(v.y) & M),
+                       v.z - __uint_as_float(__float_as_uint(v.z) & M), v.w - __uint_as_float(__float_as_uint(v.w) & M));
 }
 
-template <int BN, int NST, bool BPRE>   // BPRE: B arrives pre-split (hi, lo tensor maps)
+template <int BN, int NST, bool BPRE>   // BPRE: B's lo half arrives precomputed (its own tensor map)
 __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                               const __grid_constant__ CUtensorMap mapB,
                                                               const __grid_constant__ CUtensorMap mapBlo,
                                                               int P, int K, int CRS, long long M,
                                                               float* __restrict__ y, int relu) {
-    constexpr int A_BYTES = TM * TBK * 4;            // one of raw/hi, lo
+    constexpr int A_BYTES = TM * TBK * 4;            // raw A tile (its hi / lo go to TMEM)
     constexpr int B_BYTES = BN * TBK * 4;
-    constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+    constexpr int BOFF = A_BYTES;                    // B (hi, lo) after A
+    constexpr int STAGE = BOFF + 2 * B_BYTES;
     constexpr int HALF = BN / 2;                     // columns per drain warp
     // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = 128
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 
+    // A (raw = hi, and lo) of every stage lives in TMEM next to the two accumulator buffers:
+    // stage s at columns 2*BN + 64 s (hi) and + 32 (lo); the MMAs read only B from smem
+    constexpr unsigned TCOLS = 512;
+    static_assert(2 * BN + 64 * NST <= 512, "TMEM: accumulators + A stages");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned stage base (TMA destinations need 128 B; the allocation has +1 KB)
     unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -105,7 +131,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
 
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     ::"r"(smem_u32(&tmem_base_s)), "r"((unsigned)(2 * BN)) : "memory");
+                     ::"r"(smem_u32(&tmem_base_s)), "r"(TCOLS) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
@@ -140,8 +166,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                     unsigned char* st = smem + s * STAGE;
                     mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
                     tma_load_2d(st, &mapA, kb * TBK, m0, &full[s]);
-                    tma_load_2d(st + 2 * A_BYTES, &mapB, kb * TBK, n0, &full[s]);
-                    if (BPRE) tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mapBlo, kb * TBK, n0, &full[s]);
+                    tma_load_2d(st + BOFF, &mapB, kb * TBK, n0, &full[s]);
+                    if (BPRE) tma_load_2d(st + BOFF + B_BYTES, &mapBlo, kb * TBK, n0, &full[s]);
                 }
             }
         }
@@ -163,18 +189,18 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
                 const unsigned dt = tmem + (unsigned)(b * BN);
 #pragma unroll
                 for (int ks = 0; ks < TBK / 8; ks++) {
-                    const uint64_t ahi = umma_desc_sw128(sa + 32 * ks);
-                    const uint64_t alo = umma_desc_sw128(sa + A_BYTES + 32 * ks);
-                    const uint64_t bhi = umma_desc_sw128(sa + 2 * A_BYTES + 32 * ks);
-                    const uint64_t blo = umma_desc_sw128(sa + 2 * A_BYTES + B_BYTES + 32 * ks);
-                    const uint64_t da[3] = {ahi, ahi, alo}, db[3] = {bhi, blo, bhi};
+                    const unsigned ahi = tmem + (unsigned)(2 * BN + 64 * s + 8 * ks), alo = ahi + 32;
+                    const uint64_t bhi = umma_desc_sw128(sa + BOFF + 32 * ks);
+                    const uint64_t blo = umma_desc_sw128(sa + BOFF + B_BYTES + 32 * ks);
+                    const unsigned ta[3] = {ahi, ahi, alo};
+                    const uint64_t db[3] = {bhi, blo, bhi};
 #pragma unroll
                     for (int t = 0; t < 3; t++) {
                         const unsigned acc = (!first || ks > 0 || t > 0) ? 1u : 0u;
                         asm volatile(
                             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
-                            ::"r"(dt), "l"(da[t]), "l"(db[t]), "r"(IDESC), "r"(acc) : "memory");
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+                            ::"r"(dt), "r"(ta[t]), "l"(db[t]), "r"(IDESC), "r"(acc) : "memory");
                     }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -187,31 +213,37 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
             }
         }
     } else if (warp < 2 + NCONV / 32) {
-        // ---- converter warps: split every landed stage into hi (in place) and lo
+        // ---- converter warps: the lo half of every landed stage (the raw values serve as hi)
         const int ct = tid - 64;
         const long long gtot = ((ntile_total - blockIdx.x + gridDim.x - 1) / gridDim.x) * nk;
         for (long long g = 0; g < gtot; g++) {
             const int s = (int)(g % NST);
             mbar_wait(&full[s], (unsigned)((g / NST) & 1));
             unsigned char* st = smem + s * STAGE;
-            float4* a = reinterpret_cast<float4*>(st);
-            float4* alo = reinterpret_cast<float4*>(st + A_BYTES);
-            float4* bb = reinterpret_cast<float4*>(st + 2 * A_BYTES);
-            float4* blo = reinterpret_cast<float4*>(st + 2 * A_BYTES + B_BYTES);
+            float4* bb = reinterpret_cast<float4*>(st + BOFF);
+            float4* blo = reinterpret_cast<float4*>(st + BOFF + B_BYTES);
+            {   // thread = A row m (its warp's TMEM lane quarter): the row's 32 CRS values from the
+                // SW128 tile (16-byte chunk j of row m sits at chunk j ^ (m & 7)) -> TMEM hi, lo
+                const int m = 32 * (warp & 3) + lane;
+                const unsigned char* row = st + m * 128;
+                uint32_t h[32], l[32];
 #pragma unroll
-            for (int i = ct; i < A_BYTES / 16; i += NCONV) {
-                float4 v = a[i], lo;
-                split4(v, lo);
-                a[i] = v;
-                alo[i] = lo;
+                for (int j = 0; j < 8; j++) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (m & 7)) << 4));
+                    const float4 lv = lo_of(v);
+                    h[4 * j] = __float_as_uint(v.x); h[4 * j + 1] = __float_as_uint(v.y);
+                    h[4 * j + 2] = __float_as_uint(v.z); h[4 * j + 3] = __float_as_uint(v.w);
+                    l[4 * j] = __float_as_uint(lv.x); l[4 * j + 1] = __float_as_uint(lv.y);
+                    l[4 * j + 2] = __float_as_uint(lv.z); l[4 * j + 3] = __float_as_uint(lv.w);
+                }
+                const unsigned ta = tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(2 * BN + 64 * s);
+                tmem_st32(ta, h);
+                tmem_st32(ta + 32, l);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             }
 #pragma unroll
-            for (int i = ct; i < (BPRE ? 0 : B_BYTES / 16); i += NCONV) {
-                float4 v = bb[i], lo;
-                split4(v, lo);
-                bb[i] = v;
-                blo[i] = lo;
-            }
+            for (int i = ct; i < (BPRE ? 0 : B_BYTES / 16); i += NCONV) blo[i] = lo_of(bb[i]);
             fence_proxy_async();       // generic smem writes -> visible to the tensor core
             mbar_arrive(&conv[s]);
         }
@@ -263,7 +295,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((unsigned)(2 * BN)) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
 }
 
 int sm_count_tc() {
@@ -303,22 +335,20 @@ bool make_map(CUtensorMap* map, const float* base, long long rows, int cols, int
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// hi = x with the 13 low mantissa bits cleared, lo = x - hi, over the K x CRS weights (once
-// per call, so the GEMM's split warps only split A)
-__global__ void __launch_bounds__(256) split_b_kernel(const float* __restrict__ w, float* __restrict__ hi,
-                                                      float* __restrict__ lo, long long n) {
+// lo = x - hi (hi = x with the 13 low mantissa bits cleared) over the K x CRS weights, once
+// per call, so the GEMM's split warps only handle A; the raw weights serve as B hi
+__global__ void __launch_bounds__(256) split_b_kernel(const float* __restrict__ w, float* __restrict__ lo,
+                                                      long long n) {
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
         const float v = w[i];
-        const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-        hi[i] = h;
-        lo[i] = v - h;
+        lo[i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }
 }
 
 template <int BN, int NST>
 cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float* W, float* bsplit, float* y,
                    int relu, cudaStream_t st) {
-    constexpr int STAGE = 2 * TM * TBK * 4 + 2 * BN * TBK * 4;
+    constexpr int STAGE = TM * TBK * 4 + 2 * BN * TBK * 4;
     const size_t smem = (size_t)NST * STAGE + 1024;
     static bool attr[2] = {false, false};
     const bool pre = bsplit != nullptr;
@@ -333,9 +363,9 @@ cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float*
     if (!make_map(&ma, A, M, CRS, TM)) return cudaErrorNotSupported;
     if (pre) {
         const long long n = (long long)K * CRS;
-        float *hi = bsplit, *lo = bsplit + n;
-        split_b_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(W, hi, lo, n);
-        if (!make_map(&mb, hi, K, CRS, BN) || !make_map(&mblo, lo, K, CRS, BN)) return cudaErrorNotSupported;
+        float* lo = bsplit;
+        split_b_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(W, lo, n);
+        if (!make_map(&mb, W, K, CRS, BN) || !make_map(&mblo, lo, K, CRS, BN)) return cudaErrorNotSupported;
     } else {
         if (!make_map(&mb, W, K, CRS, BN)) return cudaErrorNotSupported;
         mblo = mb;
@@ -367,8 +397,8 @@ cudaError_t launch_tc_gemm(const Geom& g, const float* w, const float* A, float*
     if (reinterpret_cast<uintptr_t>(bsplit) & 15) bsplit = nullptr;
     // N tile: 128 unless the grid would leave SMs idle with it
     const long long mt = ((long long)g.N * P + TM - 1) / TM;
-    if (K <= 64 || mt * ((K + 127) / 128) < 148) return run_tc<64, 4>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
-    return run_tc<128, 3>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
+    if (K <= 64 || mt * ((K + 127) / 128) < 148) return run_tc<64, SPC_TC_NST64>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
+    return run_tc<128, SPC_TC_NST128>(P, K, CRS, g.N, A, w, bsplit, y, relu, st);
 }
 
 }  // namespace spc
