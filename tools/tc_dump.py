@@ -1,3 +1,8 @@
+"""Dump tcgen05 im2col outputs of a few layers to an .npz (A/B of GEMM variants: run with and
+without SPC_LIB_OVERRIDE, then compare the files bit for bit).
+
+  python tools/tc_dump.py out.npz
+"""
 import sys, os
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch, numpy as np
