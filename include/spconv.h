@@ -150,7 +150,7 @@ size_t spc_im2col_ws_bytes(const spc_conv_desc *d);
 /* GEMM engines of the dense baseline.  im2col_conv_forward uses the process-wide
  * default (spc_set_im2col_gemm; initially SPC_GEMM_AUTO: the tcgen05 3xTF32 kernel for
  * layers of >= 2^28 MACs, or >= 2^26 MACs over >= 20 output tiles of 128 positions x 64
- * (K <= 64) or 128 channels, with C*R*S % 4 == 0 (its TMA row pitches), cuBLAS FP32 otherwise,
+ * (K <= 64) or 128 channels or with C*R*S >= 2048, with C*R*S % 4 == 0 (its TMA row pitches), cuBLAS FP32 otherwise,
  * both within the 1e-4 tolerance).  SPC_GEMM_TC_3XTF32 also falls back to cuBLAS FP32
  * when C*R*S % 4 != 0.  An engine the
  * loaded cuBLAS lacks makes im2col_conv_forward return SPC_EUNSUPPORTED (BF16X9

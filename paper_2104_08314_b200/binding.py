@@ -92,7 +92,7 @@ GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32
               2: "cuBLAS FP32 emulated by 3 bf16 terms on tensor cores (CUBLAS_COMPUTE_32F_EMULATED_16BFX9)",
               3: "cuBLAS TF32 tensor cores (CUBLAS_COMPUTE_32F_FAST_TF32, 1 term)",
               4: "tcgen05 3xTF32 (this library: fp32 from three TF32 products, TMEM accumulators)",
-              5: "auto: tcgen05 3xTF32 for layers >= 2^28 MACs or >= 2^26 MACs over >= 20 tiles "
+              5: "auto: tcgen05 3xTF32 for layers >= 2^28 MACs or >= 2^26 MACs over >= 20 tiles or CRS >= 2048 "
                  "(C*R*S % 4 == 0), cuBLAS FP32 otherwise"}
 
 

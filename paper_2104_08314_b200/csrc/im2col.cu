@@ -16,16 +16,17 @@ static int g_gemm = SPC_GEMM_AUTO;   // im2col GEMM engine (spc_set_im2col_gemm)
 
 // The engine a layer actually runs: AUTO picks the tcgen05 kernel for layers of >= 2^28
 // MACs, or >= 2^26 MACs spread over >= 20 output tiles (128 positions x 64 / 128 channels)
-// -- measured (lowering + GEMM, graph, L2 flushed): cfg2 (1.2e8 MACs, 25 tiles) 26.7 vs
-// 28.7 us for cuBLAS FP32, cfg3 61 vs 98; Inception 1x3 @8 (2.3e8 MACs, 12 tiles) 41 vs 39,
-// cfg1 (4.5e5 MACs) 16 vs 12.
+// or with long tiles (C*R*S >= 2048) -- measured (lowering + GEMM, graph, L2 flushed):
+// cfg2 (1.2e8 MACs, 25 tiles) 26.7 vs 28.7 us for cuBLAS FP32, cfg3 s2 (2.3e8, 8 tiles,
+// CRS 2304) 61 vs 68, cfg3 61 vs 98; Inception 1x3 @8 (2.3e8 MACs, 12 tiles, CRS 1152)
+// 41 vs 39, cfg1 (4.5e5 MACs) 16 vs 12.
 static int effective_engine(const Geom& g) {
     if (g_gemm != SPC_GEMM_AUTO) return g_gemm;
     const double macs = (double)g.N * g.Oh * g.Ow * g.K * g.C * g.R * g.S;
     const long long mt = ((long long)g.N * g.Oh * g.Ow + 127) / 128, bn = g.K <= 64 ? 64 : 128;
     const long long tiles = mt * ((g.K + bn - 1) / bn);
-    return (macs >= 268435456.0 || (macs >= 67108864.0 && tiles >= 20)) ? SPC_GEMM_TC_3XTF32
-                                                                        : SPC_GEMM_CUBLAS_FP32;
+    const bool mid = macs >= 67108864.0 && (tiles >= 20 || g.C * g.R * g.S >= 2048);
+    return (macs >= 268435456.0 || mid) ? SPC_GEMM_TC_3XTF32 : SPC_GEMM_CUBLAS_FP32;
 }
 
 // Block (32, 8): threadIdx.x strides 32 consecutive output positions of a lowered row

@@ -80,7 +80,7 @@ def test_binding_refuses_cpu_tensors(lib):
 
 def test_im2col_engine_resolution(lib):
     """SPC_GEMM_AUTO (the default) picks the tcgen05 3xTF32 kernel for layers of >= 2^28 MACs,
-    or >= 2^26 MACs over >= 20 output tiles, whose C*R*S is a multiple of 4 (TMA row
+    or >= 2^26 MACs over >= 20 output tiles or with C*R*S >= 2048, whose C*R*S is a multiple of 4 (TMA row
     pitches), cuBLAS FP32 otherwise; an explicit
     TC_3XTF32 falls back to cuBLAS FP32 when C*R*S % 4 != 0 (include/spconv.h)."""
     prev = lib.spc_get_im2col_gemm()
@@ -90,6 +90,8 @@ def test_im2col_engine_resolution(lib):
         mid = _d(N=1, C=64, H=56, W=56, K=64)             # cfg2: 1.2e8 MACs, 25 tiles
         few = _d(N=8, C=384, H=8, W=8, K=384, R=1, S=3, pad_top=0, pad_bottom=0)   # 2.3e8 MACs, 12 tiles
         small = _d(N=1, C=16, H=14, W=14, K=16)           # cfg1: 4.5e5 MACs
+        deep = _d(N=8, C=256, H=14, W=14, K=256, stride_h=2, stride_w=2)   # cfg3 s2: 8 tiles, CRS 2304
+        assert lib.spc_im2col_engine(deep) == lib.SPC_GEMM_TC_3XTF32
         odd = _d(N=32, C=65, H=56, W=56, K=64)            # CRS = 585
         assert lib.spc_im2col_engine(big) == lib.SPC_GEMM_TC_3XTF32
         assert lib.spc_im2col_engine(mid) == lib.SPC_GEMM_TC_3XTF32
