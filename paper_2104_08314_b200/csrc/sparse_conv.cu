@@ -1284,7 +1284,12 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    // PDL (the prologue overlaps the encoder's tail) gains 1-3 us on most layers, but an
+    // 8-CTA-cluster grid larger than the SM count launched early next to a full encoder grid
+    // lost 13 us (cfg3 s2: 50.3 vs 36.9 us per step, measured with and without), so such
+    // grids launch after the encoder instead.
+    const bool pdl = !(cg >= 8 && (long long)grid.x * grid.y * grid.z > sm_count());
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL>, a);
 }
 
