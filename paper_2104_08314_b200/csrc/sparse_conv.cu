@@ -1204,10 +1204,13 @@ static size_t strip_smem(const ConvArgs& a) {
 
 // Channel split across a cluster: the largest cg in {1,2,4,8} that keeps the
 // grid within ~one wave of resident CTAs and at least 8 channels per CTA.
+// Cluster split of the input channels: the largest cg in {2, 4, 8} whose grid still fits
+// one wave, with >= 2 channels per CTA (cfg1, C = 16: cg 8 steps in 18.6 us vs 20.5 at cg 2;
+// a floor of 8 channels per CTA used to hold it at 2).
 static int pick_cg(long long ctas, int C, int per_sm) {
     int best = 1;
     for (int cg = 2; cg <= 8; cg *= 2)
-        if (ctas * cg <= 148LL * per_sm && C >= 8 * cg) best = cg;
+        if (ctas * cg <= 148LL * per_sm && C >= 2 * cg) best = cg;
     return best;
 }
 
