@@ -392,7 +392,8 @@ def test_im2col_tf32_engine_runs():
 
 @pytest.mark.parametrize("shape", [(1, 64, 56, 56, 64, 1), (2, 256, 14, 14, 256, 1), (2, 128, 28, 28, 128, 2),
                                    (1, 5, 9, 11, 70, 1), (2, 3, 17, 17, 33, 1), (3, 512, 7, 7, 512, 1),
-                                   (3, 4, 9, 11, 70, 1), (5, 8, 13, 10, 200, 2)])
+                                   (3, 4, 9, 11, 70, 1), (5, 8, 13, 10, 200, 2),
+                                   (2, 64, 16, 16, 64, 1), (2, 256, 16, 16, 256, 1)])   # M, CRS tile exactly
 def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
     """tcgen05 3xTF32 baseline GEMM vs the FP64 oracle on ragged shapes (P, K, CRS not tile
     multiples; CRS % 4 != 0 runs the cuBLAS FP32 fallback).  The TMEM accumulator is drained into
