@@ -1287,11 +1287,14 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    // PDL (the prologue overlaps the encoder's tail) gains 1-3 us on most layers, but an
-    // 8-CTA-cluster grid larger than the SM count launched early next to a full encoder grid
-    // lost 13 us (cfg3 s2: 50.3 vs 36.9 us per step, measured with and without), so such
-    // grids launch after the encoder instead.
-    const bool pdl = !(cg >= 8 && (long long)grid.x * grid.y * grid.z > sm_count());
+    // PDL (the prologue overlaps the encoder's tail) gains 1-3 us on most layers, but two
+    // kinds of grid placed early next to a full encoder grid lose: an 8-CTA-cluster grid
+    // larger than the SM count (cfg3 s2: 50.3 vs 36.9 us per step, measured with and
+    // without) and the balanced mode at one persistent CTA per SM (its equal-work ranges
+    // assume equal start times; cfg5-L0 216 vs 213 us, L1 248 vs 246).  Those launch after
+    // the encoder instead.
+    const long long ctas = (long long)grid.x * grid.y * grid.z;
+    const bool pdl = !(cg >= 8 && ctas > sm_count()) && !(BAL && ctas <= sm_count());
     cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL>, a);
 }
