@@ -20,7 +20,13 @@
  *    outputs y are NKHW fp32 with Oh = floor((H+pt+pb-R)/sh)+1 and
  *    Ow = floor((W+pl+pr-S)/sw)+1 (reading A14).
  *  - Thread safety: calls on different streams with disjoint buffers and
- *    workspaces may run concurrently.
+ *    workspaces may run concurrently.  Kernels go to the caller's CURRENT
+ *    device (cudaSetDevice); launch caches (shared-memory attributes, SM
+ *    counts) are kept per device.  Kernels whose CTAs wait on one another
+ *    (the encoder's cross-tile prefix, the balanced-mode convolution) are
+ *    launched cooperatively, so the driver co-schedules the whole grid even
+ *    when other streams hold SMs; their waits are bounded and a timeout is
+ *    reported through the encoding's overflow word (never a trap or a hang).
  */
 #ifndef SPCONV_H
 #define SPCONV_H
@@ -99,8 +105,11 @@ typedef struct {
 spc_status spc_encode_capacity(const spc_conv_desc *d, int64_t *ptr_cap, int64_t *da_cap,
                                int64_t *in_cap, size_t *ws_bytes);
 
-/* Host, synchronous.  Zero a workspace once after allocation.  Encoders leave
- * their scratch state zeroed when they complete, so this is needed only once. */
+/* Host, synchronous.  Zero a workspace once after allocation.  The encoder's
+ * cross-tile state in it is epoch-tagged (tags and counters are per launch, a
+ * consumed conv flag is re-zeroed by its consumer), so it is never reset between
+ * launches -- and must NOT be re-zeroed, or shared by two streams, in the middle
+ * of a sequence of launches: one workspace serves one stream at a time. */
 spc_status spc_workspace_init(void *ws, size_t ws_bytes, void *stream);
 
 /* CPO encoding (Alg. 1; SI Alg. 5 for S = 1)
@@ -108,8 +117,8 @@ spc_status spc_workspace_init(void *ws, size_t ws_bytes, void *stream);
  * R, S and the pads, never on the stride or K (reading A15).  One launch.
  * Unsupported (SPC_EUNSUPPORTED): R = S = 1 (pointwise);
  * S > 1 with pad_left != pad_right or pad_left > S-1 or Wp < 2S-1; S = 1 with
- * horizontal padding; pad_top or pad_bottom > R-1; a plane larger than the
- * encoder's shared-memory stage (H*W*4 > 200 KB).
+ * horizontal padding; pad_top or pad_bottom > R-1; K_h > 32; a plane larger than
+ * the encoder's shared-memory stage (H*W*4 > 192 KB = 196608 bytes).
  * ws: >= ws_bytes from spc_encode_capacity, zeroed once (spc_workspace_init). */
 spc_status cpo_encode(const spc_conv_desc *d, const float *x, spc_encoding *out, void *ws,
                       size_t ws_bytes, void *stream);
@@ -183,10 +192,35 @@ spc_status select_layer_algo(const spc_conv_desc *d, const float *samples, int32
                              size_t ws_bytes, void *stream);
 size_t spc_select_ws_bytes(const spc_conv_desc *d);
 
+/* Host, no GPU work: the selection rule of select_layer_algo applied to recorded times
+ * (replay, SPEC.md:657 / :741: the plan is the argmin on the profiling data).
+ * times_ms = {im2col, CPO, CPS} (any consistent unit); sparse_ok = 0 restricts the choice
+ * to im2col (times_ms[1..2] ignored).  Modes as spc_mode; ties prefer the
+ * smaller footprint, CPS over CPO over im2col (reading A24).  SPC_EINVAL for negative or
+ * NaN times in the considered set or an unknown mode. */
+spc_status spc_select_from_times(const float *times_ms, int32_t sparse_ok, spc_mode mode, spc_algo *choice);
+
+/* Host: output extents Oh = floor((H+pt+pb-R)/sh)+1, Ow = floor((W+pl+pr-S)/sw)+1
+ * (reading A14) -- the dims every entry point uses for y. */
+spc_status spc_output_dims(const spc_conv_desc *d, int32_t *oh, int32_t *ow);
+
 /* Host, synchronising: copy the device `lengths` of an encoding to
  * out_host[3] = {ptr_len, da_len, in_len}; returns SPC_ECAPACITY if the
- * encoder reported an overflow. */
+ * encoder reported an overflow (overflow word bit 0), SPC_ECUDA if a bounded
+ * device-side wait timed out (bit 1: encoder, bit 2: balanced-mode conv). */
 spc_status spc_encoding_lengths(const spc_encoding *enc, int64_t out_host[3], void *stream);
+
+/* Host, synchronising; a debug validator, off the hot path.  Checks
+ * that `enc` is a well-formed canonical CPO / CPS encoding for `d` (DESIGN.md Appendix A):
+ * side tables monotone and equal to the device lengths; ptr block sequence, tags, NPC /
+ * NPF placement, -1 exactly where a partition owns no column of the type, non-decreasing
+ * counts adding up to each channel's NZEs; IN local columns / rows inside the real rows,
+ * rows ascending per column; CPS set4 pairs decoding to the block's NZE count; DA values
+ * non-zero and finite.  Returns SPC_ECORRUPT (message names the first bad channel
+ * segment and the reason), SPC_ECAPACITY / SPC_ECUDA for a flagged encoding, SPC_OK
+ * otherwise.  scratch: >= 16 bytes of device memory (overwritten). */
+spc_status spc_validate_encoding(const spc_conv_desc *d, const spc_encoding *enc, void *scratch,
+                                 size_t scratch_bytes, void *stream);
 
 /* Thread-local message describing the last non-OK status of this thread. */
 const char *spc_last_error(void);

@@ -67,6 +67,9 @@ _sigs = {
     "select_layer_algo": [_D, _vp, _i32, _vp, _i32, _i32, ctypes.POINTER(_i32),
                           ctypes.POINTER(ctypes.c_float), _vp, _sz, _vp],
     "spc_encoding_lengths": [_E, ctypes.POINTER(_i64), _vp],
+    "spc_validate_encoding": [_D, _E, _vp, _sz, _vp],
+    "spc_select_from_times": [ctypes.POINTER(ctypes.c_float), _i32, _i32, ctypes.POINTER(_i32)],
+    "spc_output_dims": [_D, ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
 }
 for _n, _a in _sigs.items():
     getattr(_lib, _n).argtypes = _a
@@ -144,11 +147,14 @@ def make_desc(d: dict) -> spc_conv_desc:
                                                "pad_top", "pad_bottom", "pad_left", "pad_right")))
 
 
-def out_hw(d: dict) -> tuple[int, int]:
-    """Output extents the library uses (include/spconv.h conventions)."""
-    Oh = (d["H"] + d["pad_top"] + d["pad_bottom"] - d["R"]) // d["stride_h"] + 1
-    Ow = (d["W"] + d["pad_left"] + d["pad_right"] - d["S"]) // d["stride_w"] + 1
-    return Oh, Ow
+def spc_output_dims(d: dict) -> tuple[int, int]:
+    """Output extents (Oh, Ow) the library uses for y (spc_output_dims)."""
+    oh, ow = _i32(), _i32()
+    _check(_lib.spc_output_dims(ctypes.byref(make_desc(d)), ctypes.byref(oh), ctypes.byref(ow)), "spc_output_dims")
+    return oh.value, ow.value
+
+
+out_hw = spc_output_dims
 
 
 def spc_encode_capacity(d: dict) -> tuple[int, int, int, int]:
@@ -252,6 +258,22 @@ def select_layer_algo(d: dict, samples: torch.Tensor, M: int, w: torch.Tensor, m
                                   ctypes.byref(choice), times, _ptr(ws), ws.numel(), _stream(stream)),
            "select_layer_algo")
     return choice.value, [times[0], times[1], times[2]]
+
+
+def spc_select_from_times(times_ms, sparse_ok: bool, mode: int) -> int:
+    """Replay of the selection rule on recorded {im2col, CPO, CPS} times (no GPU work)."""
+    t = (ctypes.c_float * 3)(*[float(v) for v in times_ms])
+    choice = _i32()
+    _check(_lib.spc_select_from_times(t, int(bool(sparse_ok)), int(mode), ctypes.byref(choice)),
+           "spc_select_from_times")
+    return choice.value
+
+
+def spc_validate_encoding(d: dict, enc: "Encoding", scratch: torch.Tensor, stream=None) -> None:
+    """Debug validator: raises SpcError(SPC_ECORRUPT) for a malformed encoding."""
+    _check(_lib.spc_validate_encoding(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(scratch),
+                                      scratch.numel() * scratch.element_size(), _stream(stream)),
+           "spc_validate_encoding")
 
 
 def spc_encoding_lengths(enc: Encoding, stream=None) -> tuple[int, int, int]:

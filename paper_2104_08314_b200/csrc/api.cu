@@ -9,6 +9,9 @@
 
 namespace spc {
 size_t enc_smem_bytes(const Geom& g);
+const char* validate_reason(int code);
+cudaError_t launch_validate(const Geom& g, const spc_encoding* e, void* rec_dev, cudaStream_t st,
+                            long long* bad_channel, int* code);
 }
 
 namespace {
@@ -50,6 +53,8 @@ spc_status check_sparse_geometry(const spc_conv_desc* d) {
     const int Wp = d->W + d->pad_left + d->pad_right;
     if (d->R == 1 && d->S == 1) return fail(SPC_EUNSUPPORTED, "pointwise kernels are routed to im2col (PAPER.md:123)");
     if (d->S > 8) return fail(SPC_EUNSUPPORTED, "K_w > 8 not supported");
+    // padded-frame row masks are shifted by pad_top inside 32-bit words (pad_top <= R-1 < 32)
+    if (d->R > 32) return fail(SPC_EUNSUPPORTED, "K_h > 32 not supported");
     if (d->S > 1) {
         if (d->pad_left != d->pad_right) return fail(SPC_EUNSUPPORTED, "pad_left != pad_right (reading A16)");
         if (d->pad_left > d->S - 1) return fail(SPC_EUNSUPPORTED, "pad_left >= K_w");
@@ -86,7 +91,7 @@ spc_status do_encode(const spc_conv_desc* d, const float* x, spc_encoding* out, 
     spc::Geom g = spc::make_geom(*d);
     if ((size_t)spc::ws_layout(g).cps_in > ws_bytes) return fail(SPC_EINVAL, "workspace too small");
     if (out->ptr_cap < 0 || out->da_cap < 0 || out->in_cap < 0) return fail(SPC_EINVAL, "negative capacity");
-    out->algo = (cps && d->S > 1) ? SPC_ALGO_CPS : (cps ? SPC_ALGO_CPS : SPC_ALGO_CPO);
+    out->algo = cps ? SPC_ALGO_CPS : SPC_ALGO_CPO;   // S = 1: CPS streams equal CPO (reading A13)
     out->geom = *d;
     return cuda_status(spc::launch_encode(g, cps && d->S > 1, x, out, ws, (cudaStream_t)stream), "encode");
 }
@@ -226,8 +231,37 @@ spc_status spc_encoding_lengths(const spc_encoding* enc, int64_t out_host[3], vo
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_status(e, "spc_encoding_lengths");
     out_host[0] = h[0]; out_host[1] = h[1]; out_host[2] = h[2];
+    if (h[3] & 6) return fail(SPC_ECUDA, "a bounded device-side wait timed out (overflow word %lld: bit 1 encoder, "
+                              "bit 2 balanced-mode conv)", (long long)h[3]);
     if (h[3]) return fail(SPC_ECAPACITY, "encoder overflow: needs ptr %lld da %lld in %lld", (long long)h[0],
                           (long long)h[1], (long long)h[2]);
+    return SPC_OK;
+}
+
+spc_status spc_validate_encoding(const spc_conv_desc* d, const spc_encoding* enc, void* scratch,
+                                 size_t scratch_bytes, void* stream) {
+    spc_status s = check_sparse_geometry(d);
+    if (s != SPC_OK) return s;
+    if (!enc || !scratch || scratch_bytes < 16) return fail(SPC_EINVAL, "bad argument");
+    if (!enc->ptr || !enc->da || !enc->in || !enc->chan_ptr_off || !enc->chan_nz_off || !enc->chan_in_off ||
+        !enc->lengths)
+        return fail(SPC_EINVAL, "null stream pointer in spc_encoding");
+    const spc_conv_desc& e = enc->geom;
+    if (e.N != d->N || e.C != d->C || e.H != d->H || e.W != d->W || e.R != d->R || e.S != d->S ||
+        e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom || e.pad_left != d->pad_left ||
+        e.pad_right != d->pad_right)
+        return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
+    int64_t len[3];
+    s = spc_encoding_lengths(enc, len, stream);
+    if (s != SPC_OK) return s;
+    spc::Geom g = spc::make_geom(*d);
+    long long bad = -1;
+    int code = 0;
+    s = cuda_status(spc::launch_validate(g, enc, scratch, (cudaStream_t)stream, &bad, &code), "validate");
+    if (s != SPC_OK) return s;
+    if (bad >= 0)
+        return fail(SPC_ECORRUPT, "encoding corrupt at channel segment %lld (n=%lld, c=%lld): %s", bad, bad / g.C,
+                    bad % g.C, spc::validate_reason(code));
     return SPC_OK;
 }
 
@@ -326,6 +360,15 @@ spc_status select_layer_algo(const spc_conv_desc* d, const float* samples, int32
     cudaEventDestroy(e1);
     if (r != SPC_OK) return r;
     for (int i = 0; i < 3; i++) times_ms[i] = (t[i] >= 0.f) ? t[i] / reps : -1.f;
+    return spc_select_from_times(times_ms, sparse_ok ? 1 : 0, mode, choice);
+}
+
+spc_status spc_select_from_times(const float* times_ms, int32_t sparse_ok, spc_mode mode, spc_algo* choice) {
+    if (!times_ms || !choice) return fail(SPC_EINVAL, "null pointer");
+    if (mode < SPC_FAVOUR_TIME || mode > SPC_BEST_OF_THREE) return fail(SPC_EINVAL, "unknown mode %d", (int)mode);
+    if (!(times_ms[0] >= 0.f)) return fail(SPC_EINVAL, "im2col time must be >= 0");
+    if (sparse_ok && (!(times_ms[1] >= 0.f) || !(times_ms[2] >= 0.f)))
+        return fail(SPC_EINVAL, "sparse times must be >= 0 when sparse_ok");
     // argmin; ties prefer the smaller footprint: CPS over CPO over im2col (reading A24)
     spc_algo best = SPC_ALGO_IM2COL;
     float tb = times_ms[0];
@@ -334,6 +377,16 @@ spc_status select_layer_algo(const spc_conv_desc* d, const float* samples, int32
         if (mode != SPC_FAVOUR_TIME && times_ms[2] <= tb) { best = SPC_ALGO_CPS; tb = times_ms[2]; }
     }
     *choice = best;
+    return SPC_OK;
+}
+
+spc_status spc_output_dims(const spc_conv_desc* d, int32_t* oh, int32_t* ow) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!oh || !ow) return fail(SPC_EINVAL, "null pointer");
+    const spc::Geom g = spc::make_geom(*d);
+    *oh = g.Oh;
+    *ow = g.Ow;
     return SPC_OK;
 }
 

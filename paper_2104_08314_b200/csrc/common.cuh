@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstdlib>
+
 #include "../../include/spconv.h"
 
 namespace spc {
@@ -35,7 +38,7 @@ inline Geom make_geom(const spc_conv_desc& d) {
     return g;
 }
 
-// Encoder: 8 warps per CTA; a tile = P consecutive channel planes staged in smem.
+// Encoder: 16 warps per CTA; a tile = P consecutive channel planes staged in smem.
 constexpr int kEncWarps = 16;
 constexpr int kEncMaxPlaneBytes = 192 * 1024;  // smem stage of one plane
 
@@ -49,6 +52,47 @@ struct EncState {
 };
 
 __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- per-device launch caches (host).  Kernel attributes and SM counts belong to one
+// device context, so every cache is an array indexed by the current device (the C ABI has
+// no device argument: launches go to the caller's current device).  Races between threads
+// only repeat an idempotent cudaFuncSetAttribute.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return d;
+}
+inline int device_sm_count() {
+    static std::atomic<int> n[kMaxDevices];
+    const int dev = current_device();
+    int v = n[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        n[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+// Raise cudaFuncAttributeMaxDynamicSharedMemorySize of `func` on the current device to at
+// least `bytes` (cache: one std::atomic<size_t>[kMaxDevices] per kernel instantiation).
+inline cudaError_t ensure_smem_attr(const void* func, size_t bytes, std::atomic<size_t>* cache) {
+    std::atomic<size_t>& c = cache[current_device()];
+    if (c.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c.store(bytes, std::memory_order_relaxed);
+    return e;
+}
+
+// Kernels whose CTAs wait on other CTAs of the same grid launch with
+// cudaLaunchAttributeCooperative (co-scheduled grid).  SPC_COOPERATIVE=0 disables it
+// (development A/B only).
+inline bool cooperative_launches() {
+    static const int on = [] {
+        const char* e = getenv("SPC_COOPERATIVE");
+        return (e && atoi(e) == 0) ? 0 : 1;
+    }();
+    return on != 0;
+}
 
 // upper bound on encoder tiles (one plane per tile), for workspace sizing
 inline long long enc_tiles(const Geom& g) { return g.NC; }

@@ -34,6 +34,7 @@ constexpr unsigned kBulkChunk = 1u << 15;   // bytes per cp.async.bulk
 constexpr int kTagShift = 40;
 constexpr unsigned long long kValMask = (1ull << kTagShift) - 1;
 constexpr int kTabIn = 1 << 16, kTabOk = 1 << 17;   // column-table flags (low 16 bits: local column)
+constexpr long long kSpinLimit = 1ll << 24;         // polls before a cross-tile wait gives up
 
 struct EncArgs {
     Geom g;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
     __shared__ long long s_tile_tot[3];
     __shared__ long long s_pre[3];
     __shared__ unsigned s_epoch;
+    __shared__ int s_timeout;
     __shared__ __align__(8) unsigned long long s_bar[1];
     unsigned s_phase = 0;   // (per thread) parity of the staging barrier
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
     pdl_trigger();   // the dependent convolution may launch and stage its taps
     if (threadIdx.x == 0) {
         s_epoch = *reinterpret_cast<volatile unsigned*>(&a.st->epoch);
+        s_timeout = 0;
         mbar_init(s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
                 long long spin = 0;
                 while (ld_acquire_u32(counter) < target) {
                     __nanosleep(32);
-                    if (++spin > (1ll << 24)) __trap();   // bounded: never hang the GPU
+                    if (++spin > kSpinLimit) { s_timeout = 1; break; }   // bounded: never hang the GPU
                 }
             }
         }
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
                 long long spin = 0;
                 while (((v = ld_relaxed64(a.agg + i)) >> kTagShift) != tag) {
                     if (a.multi_round) __nanosleep(64);
-                    if (++spin > (1ll << 24)) __trap();
+                    if (++spin > kSpinLimit) { s_timeout = 1; break; }
                 }
                 const long long val = (long long)(v & kValMask);
                 const int sidx = (int)(i % 3);
@@ -372,6 +375,12 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             if (lane == 0) { s_red[warp][0] = p0; s_red[warp][1] = p1; s_red[warp][2] = p2; }
         }
         __syncthreads();
+        if (s_timeout) {
+            // a predecessor never published (cannot happen with a co-resident grid): report it in
+            // the overflow word (bit 1, sticky) and leave; waiters on this tile time out as well
+            if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned long long*>(a.lengths + 3), 2ull);
+            return;
+        }
         if (threadIdx.x < 3) {
             long long s = 0;
             for (int w = 0; w < kEncWarps; w++) s += s_red[w][threadIdx.x];
@@ -389,7 +398,11 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             a.lengths[0] = t0;
             a.lengths[1] = t1;
             a.lengths[2] = t2;
-            a.lengths[3] = (t0 > a.cap_ptr || t1 > a.cap_da || t2 > a.cap_in) ? 1 : 0;
+            // bit 0: capacity overflow of this launch; bits 1-2 (wait timeouts) are sticky
+            unsigned long long* ov = reinterpret_cast<unsigned long long*>(a.lengths + 3);
+            const unsigned long long o = (t0 > a.cap_ptr || t1 > a.cap_da || t2 > a.cap_in) ? 1ull : 0ull;
+            atomicAnd(ov, ~1ull);
+            if (o) atomicOr(ov, o);
             a.st->count[(s_epoch + 1u) & 1u] = 0;   // the next launch's counter (unused in this one)
             a.st->epoch = s_epoch + 1u;
         }
@@ -617,16 +630,7 @@ struct EncPlan {
     size_t smem;
 };
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count() { return device_sm_count(); }
 
 // Tile size: prefer 2 resident CTAs per SM (tiles within ~110 KB of smem), else 1; take
 // the fewest rounds that largest tile allows, then the smallest P that still needs only
@@ -673,14 +677,13 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
     a.P = pl.P;
     a.ntiles = pl.ntiles;
     void (*kern)(EncArgs) = cps ? encode_kernel<true> : encode_kernel<false>;
-    static size_t attr_bytes[2] = {0, 0};
-    if (attr_bytes[cps] < pl.smem) {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    static std::atomic<size_t> attr_bytes[2][kMaxDevices];
+    {
+        cudaError_t err = ensure_smem_attr((const void*)kern, pl.smem, attr_bytes[cps]);
         if (err != cudaSuccess) return err;
-        attr_bytes[cps] = pl.smem;
     }
     // the cross-tile prefix needs every CTA resident: cap the grid at the
-    // occupancy limit (CTAs then loop over tiles in increasing order)
+    // occupancy limit (CTAs then loop over tiles in increasing order) and launch cooperatively
     int occ = 0;
     cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, pl.smem);
     if (err != cudaSuccess) return err;
@@ -692,11 +695,15 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    // cooperative: the driver co-schedules every CTA of the grid (the cross-tile prefix waits
+    // on other CTAs), even when kernels on other streams hold SMs
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cooperative_launches() ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

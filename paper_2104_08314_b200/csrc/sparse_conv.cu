@@ -295,12 +295,14 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
                                                          const int64_t* __restrict__ cpo_off,
                                                          const int64_t* __restrict__ cnz_off,
                                                          const int64_t* __restrict__ cin_off,
-                                                         int32_t* __restrict__ out) {
+                                                         int32_t* __restrict__ out,
+                                                         const unsigned long long* status) {
     __shared__ int s_cnt[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long nc = blockIdx.x;
     pdl_wait();
     pdl_trigger();
+    if (*reinterpret_cast<volatile const unsigned long long*>(status) != 0ull) return;   // flagged encoding
     const long long Z = cnz_off[nc], Q = cin_off[nc];
     const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q);
     if (nnz == 0) return;
@@ -348,7 +350,8 @@ cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, cps_expand_kernel, g, (const int32_t*)e->ptr, (const int32_t*)e->in,
                               (const int64_t*)e->chan_ptr_off, (const int64_t*)e->chan_nz_off,
-                              (const int64_t*)e->chan_in_off, in_cpo);
+                              (const int64_t*)e->chan_in_off, in_cpo,
+                              (const unsigned long long*)(e->lengths + 3));
 }
 
 // ------------------------------------------------------------ conv kernels
@@ -382,6 +385,8 @@ struct ConvArgs {
                     // the balanced mode's published partials (or null)
     size_t scratch_bytes;
     unsigned* sk_flags;   // balanced mode: one "partial published" flag per CTA (zeroed after use)
+    unsigned long long* status;   // the encoding's overflow word (lengths[3]): nonzero -> y = 0;
+                                  // a balanced-mode wait timeout sets bit 2
     int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
     int sk_strips;        // balanced mode: column strips per image (unit = (k-block, image, strip))
     long long sk_units;   // balanced mode: strips x images x k-blocks
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     // barrier of each segment.
     __shared__ int s_seg[2];
     int t_next = 0;
+    bool bad = false;
     if constexpr (BAL) {
         if (threadIdx.x == 0) {
             s_seg[0] = sk_start<T>(a, blockIdx.x);
@@ -694,14 +700,20 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             probe(1);
             pdl_wait();
             probe(2);
+            // an encoding the encoder flagged (capacity overflow / wait timeout) is not read:
+            // the unit's output is written as zeros (all threads read the same word)
+            if (*reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull) {
+                bad = true;
+                cp_async_wait_all();   // the prologue's tap copies land before smem is reused
+            }
         }
         int buf = 0;
-        if (c_begin < c_end) {
+        if (c_begin < c_end && !bad) {
             stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
             if (BAL && threadIdx.x == 0) s_seg[0] = t_next;
             stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
         }
-        for (int c0 = c_begin; c0 < c_end; c0 += CHS, buf ^= 1) {
+        for (int c0 = c_begin; c0 < c_end && !bad; c0 += CHS, buf ^= 1) {
             const int chn = min(CHS, c_end - c0);
             const bool stage = !(dev_phase_mode() == 1 && !(first && c0 == c_begin));
             // ---- P0: taps (cp.async, with this chunk's prefetched ptr segments in flight); zero the windows
@@ -1002,8 +1014,16 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     int sb = sk_start<T>(a, blockIdx.x + 1);
                     for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
                         const int sn = sk_start<T>(a, b + 1);
-                        if (sn > sb)
-                            while (ld_acquire32(a.sk_flags + b) == 0u) __nanosleep(64);
+                        if (sn > sb) {
+                            long long spin = 0;
+                            while (ld_acquire32(a.sk_flags + b) == 0u) {
+                                __nanosleep(64);
+                                if (++spin > (1ll << 24)) {   // bounded (co-scheduled grid: unreachable)
+                                    atomicOr(a.status, 4ull);
+                                    break;
+                                }
+                            }
+                        }
                         sb = sn;
                     }
                 }
@@ -1153,7 +1173,8 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
     for (int i = 0; i < kGenTY * kGenTX; i++) acc[i * 32 + lane] = 0.f;
     const int k = kbase + lane;
     pdl_wait();
-    for (int c = warp; c < g.C; c += kGenWarps) {
+    const bool bad = *reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull;   // flagged: y = 0
+    for (int c = warp; c < g.C && !bad; c += kGenWarps) {
         const long long nc = (long long)n * g.C + c;
         ChanDir d;
         const int32_t* seg = a.ptr + a.cpo_off[nc];
@@ -1240,15 +1261,7 @@ static bool balance_enabled() {
     return !env || atoi(env) != 0;
 }
 
-static int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            n = 148;
-    }
-    return n;
-}
+static int sm_count() { return device_sm_count(); }
 template <class T>
 static StripPlan<T> plan_strip(const Geom& g) {
     StripPlan<T> p;
@@ -1268,18 +1281,17 @@ static StripPlan<T> plan_strip(const Geom& g) {
 
 template <class T, bool BAL>
 static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t smem, cudaStream_t st) {
-    static size_t attr_bytes = 0;     // per instantiation
-    if (attr_bytes < smem) {
-        cudaError_t err = cudaFuncSetAttribute(strip_conv_kernel<T, BAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static std::atomic<size_t> attr_bytes[kMaxDevices];     // per instantiation and device
+    {
+        cudaError_t err = ensure_smem_attr((const void*)strip_conv_kernel<T, BAL>, smem, attr_bytes);
         if (err != cudaSuccess) return err;
-        attr_bytes = smem;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(32 * a.rt * a.csplit);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
@@ -1296,6 +1308,12 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
     const long long ctas = (long long)grid.x * grid.y * grid.z;
     const bool pdl = !(cg >= 8 && ctas > sm_count()) && !(BAL && ctas <= sm_count());
     cfg.numAttrs = pdl ? 2 : 1;
+    if (BAL && cooperative_launches()) {
+        // the balanced mode's CTAs wait on one another: co-scheduled grid (cluster size 1 here)
+        attr[cfg.numAttrs].id = cudaLaunchAttributeCooperative;
+        attr[cfg.numAttrs].val.cooperative = 1;
+        cfg.numAttrs++;
+    }
     return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL>, a);
 }
 
@@ -1390,6 +1408,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.wp = w_packed;
     a.y = y;
     a.relu = relu;
+    a.status = reinterpret_cast<unsigned long long*>(e->lengths + 3);
     a.tiles_x = 1;
     a.cg = 1;
     a.rt = 1;

@@ -298,15 +298,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) tc_gemm_kernel(const __grid_const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
 }
 
-int sm_count_tc() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-            n = 148;
-    }
-    return n;
-}
+int sm_count_tc() { return device_sm_count(); }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -350,13 +342,12 @@ cudaError_t run_tc(int P, int K, int CRS, int nimg, const float* A, const float*
                    int relu, cudaStream_t st) {
     constexpr int STAGE = TM * TBK * 4 + 2 * BN * TBK * 4;
     const size_t smem = (size_t)NST * STAGE + 1024;
-    static bool attr[2] = {false, false};
+    static std::atomic<size_t> attr[2][kMaxDevices];
     const bool pre = bsplit != nullptr;
-    if (!attr[pre]) {
-        cudaError_t e = cudaFuncSetAttribute(pre ? tc_gemm_kernel<BN, NST, true> : tc_gemm_kernel<BN, NST, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr(pre ? (const void*)tc_gemm_kernel<BN, NST, true> : (const void*)tc_gemm_kernel<BN, NST, false>,
+                                         smem, attr[pre]);
         if (e != cudaSuccess) return e;
-        attr[pre] = true;
     }
     const long long M = (long long)nimg * P;
     CUtensorMap ma, mb, mblo;

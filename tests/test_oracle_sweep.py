@@ -153,3 +153,26 @@ def test_real_valued_sparse_conv_close(oracle_mod):
     for cps in (False, True):
         got = oracle_mod.sparse_conv(d, oracle_mod.encode(d, x, cps=cps), w)
         np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_direct_conv_at_equals_direct_conv_everywhere(oracle_mod):
+    """oc_direct_conv_at (Eq. 1 at chosen output coordinates) is the reference
+    of the sampled GPU parity tests: over the 400-case integer sweep (strides 1/2, asymmetric
+    H pads, 1x7 / 7x1 / 5x5 / 2x2 / 3x5, VALID / SAME / partial pads) it must equal the pinned
+    direct_conv and the independent numpy einsum on EVERY output coordinate (all boundary
+    rows / columns included), exactly; plus one real-valued case at 1e-12."""
+    for d, rho, seed in CASES:
+        x = int_map(d["N"], d["C"], d["H"], d["W"], rho, seed)
+        w = int_weights(d["K"], d["C"], d["R"], d["S"], seed)
+        ref = oracle_mod.direct_conv(d, x, w)
+        idx = np.argwhere(np.ones(ref.shape, dtype=bool))          # every (n, k, y, x)
+        got = oracle_mod.direct_conv_at(d, x, w, idx)
+        assert np.array_equal(got, ref.reshape(-1)), d
+        assert np.array_equal(got, np_conv_einsum(d, x, w).reshape(-1)), d
+    d = layer_desc(3, 16, 14, 14, 8, 3, 3, 2, 2, 1, 1, 1, 1)
+    x = clustered_relu(3, 16, 14, 14, 0.2, 3, dead_frac=0.25)
+    w = he_normal(8, 16, 3, 3, 3)
+    ref = np_conv_einsum(d, x, w)
+    rng = np.random.default_rng(7)
+    idx = np.stack([rng.integers(0, s, 500) for s in ref.shape], axis=1)
+    np.testing.assert_allclose(oracle_mod.direct_conv_at(d, x, w, idx), ref[tuple(idx.T)], rtol=1e-12, atol=1e-13)
