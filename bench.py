@@ -1,18 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark of the CPO/CPS sparse-conv hot path on B200 (contract: see DESIGN.md §Measurement).
+"""Benchmark of the CPO/CPS sparse-conv hot path on B200 (contract: see DESIGN.md §8).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3]
 
 One step = one pass of the hot path over one batch of the workload: CPO encode
-(one launch) + sparse convolution (one launch) of configs[1] (cfg2: 1x64x56x56,
-rho 0.3, 64 output channels, 3x3, s1, pad 1).  Inputs are synthetic (seeded
-clustered-ReLU, DESIGN.md §Input recipe) and resident in HBM; L2 is flushed
-between timed steps.  value = dense-equivalent GFLOP/s (2*N*K*C*R*S*Oh*Ow per
+(one launch) + sparse convolution (one launch).  The headline workload is
+BASELINE.json configs[2] (cfg3: 8x256x14x14, rho 0.1, 20% dead channels,
+256 output channels, 3x3, s1, pad 1), the largest single-layer configuration.
+Inputs are synthetic (seeded clustered-ReLU) and resident in HBM.
+L2: steps run back to back over NSET copies of the layer's buffers (input,
+encoding, workspace, packed weights, output) whose bytes touched per cycle
+exceed 1.5x the 126 MB L2, so every step reads its data cold ("inputs larger
+than L2"); configurations too small for that (cfg1) flush L2 between steps
+instead, and say so.  value = dense-equivalent GFLOP/s (2*N*K*C*R*S*Oh*Ow per
 step / device time), summed over ranks (weak scaling: every rank encodes and
-convolves its own batch; no data-path collective).  The same line carries the
-CPS path, the im2col baseline (lowering + GEMM), the compression ratio, the
-roofline of the dominant kernel, the host-buffer end-to-end number, clocks and
-the oracle timed on the host (cpu_baseline).
+convolves its own batch; no data-path collective).  The same line carries
+per-kernel launch durations, the roofline of the dominant kernel, per-config
+rows (cfg1..cfg4, the cfg3 stride-2 layer and density sweep), the im2col
+baseline, the compression ratio, the host-buffer end-to-end number, clocks,
+the cfg5 stack (offline selection and forced CPO) and the oracle timed on the
+host (cpu_baseline).
 
 --impl reference runs the CPU oracle (oracle/, plain C, FP64) as the reference
 arm on the same workload, on the host, rank 0 only.
@@ -244,22 +251,195 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------- rotating buffers
+
+L2_BYTES = 126 * 2 ** 20
+
+
+class Rotating:
+    """NSET copies of one layer's device buffers (input, encoding, workspace, packed weights,
+    output; lowered matrix for im2col) so that back-to-back steps cycle through more bytes
+    than L2 holds: every step reads its data cold without an L2 flush between steps."""
+
+    def __init__(self, d, pool: np.ndarray, w: np.ndarray, dev, min_sets=4, max_sets=128, relu=False):
+        import torch
+        from paper_2104_08314_b200.layer import SparseConvLayer
+        self.d, self.dev = d, dev
+        N = d["N"]
+        Oh, Ow = spc_out_hw(d)
+        rho = float((pool != 0).mean())
+        x_b = 4 * N * d["C"] * d["H"] * d["W"]
+        enc_b = 2 * 8 * rho * N * d["C"] * d["H"] * d["W"] + 4 * N * d["C"] * (3 + 2 * (d["W"] + 2))
+        w_b = 4 * d["K"] * d["C"] * d["R"] * d["S"]
+        y_b = 4 * N * d["K"] * Oh * Ow
+        self.touched = x_b + enc_b + w_b + y_b          # per step (encode reads x, writes enc; conv reads enc, w)
+        need = int(np.ceil(1.5 * L2_BYTES / self.touched))
+        self.cold = need <= max_sets
+        self.nset = max(min_sets, min(need, max_sets)) if self.cold else min_sets
+        self.layers, self.xs = [], []
+        nd = pool.shape[0]
+        for i in range(self.nset):
+            idx = [(i + j) % nd for j in range(N)]     # rotate the distinct images through the batch
+            self.xs.append(torch.from_numpy(np.ascontiguousarray(pool[idx])).to(dev))
+            self.layers.append(SparseConvLayer(d, torch.from_numpy(w).to(dev), device=dev, relu=relu))
+        self.flush = None if self.cold else torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+        self._graphs = {}
+
+    def graph(self, kind: str, n: int):
+        """One CUDA graph of n consecutive steps of `kind` (sets 0..n-1): step / encode / conv /
+        cps / im2col.  The host enqueues n steps at once; inside the graph the kernels run
+        back to back (PDL overlaps a conv's prologue with its encoder)."""
+        import torch
+        key = (kind, n)
+        if key in self._graphs:
+            return self._graphs[key]
+        Ls, xs = self.layers, self.xs
+
+        def body():
+            for i in range(n):
+                L, x = Ls[i % self.nset], xs[i % self.nset]
+                if kind == "step":
+                    L.forward(x, "cpo")
+                elif kind == "encode":
+                    L.encode(x, "cpo")
+                elif kind == "conv":
+                    L.conv()
+                elif kind == "cps":
+                    L.forward(x, "cps")
+                elif kind == "im2col":
+                    L.forward(x, "im2col")
+        # warm the buffers (lowered workspaces, the encodings the conv-only graph reads)
+        body()
+        torch.cuda.synchronize()
+        g = Ls[0].capture(body, warmup=1)
+        self._graphs[key] = g
+        return g
+
+    def timed(self, kind: str, steps: int, stream) -> float:
+        """Device ms of exactly `steps` steps of `kind`: back to back over the rotating sets
+        (full cycles as one graph, the remainder as a second), or -- for a configuration too
+        small to exceed L2 -- one step per replay with a 2x-L2 write between steps."""
+        import torch
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if not self.cold:
+            g = self.graph(kind, 1)
+            tot = 0.0
+            for _ in range(steps):
+                self.flush.zero_()
+                ev0.record(stream)
+                g.replay()
+                ev1.record(stream)
+                ev1.synchronize()
+                tot += ev0.elapsed_time(ev1)
+            return tot
+        full, rem = divmod(steps, self.nset)
+        gf = self.graph(kind, self.nset) if full else None
+        gr = self.graph(kind, rem) if rem else None
+        ev0.record(stream)
+        for _ in range(full):
+            gf.replay()
+        if gr is not None:
+            gr.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1)
+
+    def l2_note(self) -> str:
+        if self.cold:
+            return (f"inputs larger than L2: back-to-back steps over {self.nset} buffer sets, "
+                    f"~{self.nset * self.touched / 2**20:.0f} MiB touched per cycle (L2 126 MiB)")
+        return f"L2 flushed between steps (2x-L2 write; {self.nset} sets would not exceed L2)"
+
+
+def spc_out_hw(d):
+    import paper_2104_08314_b200 as spc
+    return spc.spc_output_dims(d)
+
+
+def make_pool(c, rank: int = 0, distinct: int = 4):
+    """Distinct seeded clustered-ReLU images of a config (each rank draws its own)."""
+    d = c["desc"]
+    nd = max(d["N"], distinct)
+    return clustered_relu(nd, d["C"], d["H"], d["W"], c["density"], c["seed"] + 7919 * rank, c["dead_frac"],
+                          c["zero_tile_frac"])
+
+
+def fp32_peak(sm_max_mhz):
+    return SM_COUNT * FP32_LANES * 2 * sm_max_mhz * 1e6 / 1e12   # TFLOP/s, derived
+
+
+def measure_layer(name, d, pool, w, dev, stream, steps, hbm_gbs, p_fp32, im2col=True, cps=True):
+    """One per-config row: encode / conv / step / CPS / im2col device times per launch (back to
+    back over rotating sets), the conv's FP32 roofline fraction, the encoder's HBM fraction,
+    the compression ratio and the exact NZE work."""
+    import paper_2104_08314_b200 as spc
+    R = Rotating(d, pool, w, dev)
+    Oh, Ow = spc_out_hw(d)
+    t = {k: R.timed(k, steps, stream) / steps * 1e3 for k in ("step", "encode", "conv")}
+    if cps:
+        t["cps_step"] = R.timed("cps", steps, stream) / steps * 1e3
+    if im2col:
+        t["im2col"] = R.timed("im2col", steps, stream) / steps * 1e3
+    L0 = R.layers[0]
+    L0.forward(R.xs[0], "cpo")
+    pl_, dl_, il_ = L0.lengths()
+    x0 = R.xs[0].cpu().numpy()
+    macs = nze_macs(d, x0, Oh, Ow)
+    flops = 2.0 * macs
+    conv_bytes = 4 * (pl_ + dl_ + il_) + 8 * 2 * (d["N"] * d["C"] + 1) + 4 * d["K"] * d["C"] * d["R"] * d["S"] + \
+        4 * d["N"] * d["K"] * Oh * Ow
+    enc_bytes = 4 * x0.size + 4 * (pl_ + dl_ + il_) + 8 * 3 * (d["N"] * d["C"] + 1)
+    s_im2col = d["N"] * Oh * Ow * d["C"] * d["R"] * d["S"]
+    t_roof = max(conv_bytes / (hbm_gbs * 1e9), flops / (p_fp32 * 1e12))
+    row = {"workload": name, "shape": {k: d[k] for k in d}, "density_measured": round(float((x0 != 0).mean()), 4),
+           "encode_us": t["encode"], "conv_us": t["conv"], "step_us": t["step"],
+           "dense_equiv_gflops": dense_flops(d, Oh, Ow) / (t["step"] * 1e-6) / 1e9,
+           "conv_fp32_frac": t_roof / (t["conv"] * 1e-6), "conv_tflops_nze": flops / (t["conv"] * 1e-6) / 1e12,
+           "encode_hbm_frac": enc_bytes / (t["encode"] * 1e-6) / 1e9 / hbm_gbs,
+           "encode_gbs": enc_bytes / (t["encode"] * 1e-6) / 1e9,
+           "cr_cpo": s_im2col / (pl_ + dl_ + il_), "nze_macs": macs, "l2": R.l2_note()}
+    if cps:
+        row["cps_step_us"] = t["cps_step"]
+    if im2col:
+        row["im2col_us"] = t["im2col"]
+        row["im2col_gemm"] = spc.GEMM_NAMES[spc.spc_im2col_engine(d)]
+        row["speedup_vs_im2col"] = t["im2col"] / t["step"]
+    return row, R
+
+
 # ---------------------------------------------------------------- cfg5 stack leg
 
-def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
+def run_stack(args, world, rank, dev, hbm_gbs, p_fp32, mode="best_of_three", force=None, S=None):
     """cfg5: global batch args.stack_batch sharded over the ranks (strong scaling of this
-    sub-metric), per-layer plan selected offline on rank 0 and broadcast, the 16 layers
-    captured in one CUDA graph, then the one output gather (NCCL all-gather).
-    images/s = global batch / max over ranks of (stack + gather) device time."""
+    sub-metric).  The per-layer plan is selected offline ONCE on rank 0 and
+    persisted to a plan file every rank reads (SURVEY §8(e): no collective carries it);
+    force="cpo" runs the method on all 16 layers instead.  The 16 layers are one CUDA
+    graph; then the one output gather.  Every layer's data exceeds L2 at this batch, so
+    steps run back to back.  images/s = global batch / max over ranks of device time."""
+    import tempfile
+
     import torch
     import torch.distributed as dist
 
     import paper_2104_08314_b200 as spc
-    from paper_2104_08314_b200.stack import Cfg5Stack, broadcast_plan, gather_outputs, shard_range
+    from paper_2104_08314_b200.stack import Cfg5Stack, gather_outputs, load_plan, save_plan, shard_range
     lo, hi = shard_range(args.stack_batch, world, rank)
-    S = Cfg5Stack(hi - lo, dev, rank=rank)
-    plan = S.select(args.stack_mode) if rank == 0 else None
-    plan = broadcast_plan(plan)
+    if S is None:
+        S = Cfg5Stack(hi - lo, dev, rank=rank)
+    names = [sp["name"] for sp in S.specs]
+    if force:
+        plan = [force] * len(S.layers)
+        plan_src = f"forced: {force} on every layer"
+    else:
+        path = args.plan_file or os.path.join(tempfile.gettempdir(),
+                                              f"spc_cfg5_plan_{mode}_{os.environ.get('MASTER_PORT', '0')}.json")
+        if rank == 0 and not args.plan_file:
+            S.select(mode)
+            save_plan(path, names, S.plan, mode, S.select_times, [sp["density"] for sp in S.specs])
+        if world > 1:
+            dist.barrier()   # control plane only: the plan travels through the file
+        plan = load_plan(path, names)
+        plan_src = f"offline selection ({mode}) on rank 0, read from plan file {os.path.basename(path)}"
     S.set_plan(plan)
     graph = S.capture()
     stream = torch.cuda.current_stream()
@@ -273,7 +453,6 @@ def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
         dist.barrier()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.stack_steps)]
     for i in range(args.stack_steps):
-        flush.zero_()
         ev[i][0].record(stream)
         graph.replay()
         ev[i][1].record(stream)
@@ -287,34 +466,50 @@ def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_stack, t_gather, t_tot = (float(v) for v in tt.tolist())
     assert out.shape[0] == args.stack_batch
+    # per-layer device time of the chosen algorithm (one graph per layer, back to back)
+    layer_ms = []
+    for L, x, algo in zip(S.layers, S.inputs, S.plan):
+        g = L.capture(lambda L=L, x=x, algo=algo: L.forward(x, algo), warmup=1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        layer_ms.append(e0.elapsed_time(e1) / 3)
+        del g
     # roofline of the chosen plan (per-layer t_roof = max(bytes / HBM, FLOPs / peak of its engine))
-    t_roof = 0.0
+    t_roof, t_roof_sparse = 0.0, 0.0
     layers = []
-    for sp, L, algo, xb in zip(S.specs, S.layers, S.plan, S.host_inputs):
+    for sp, L, algo, xb, lms in zip(S.specs, S.layers, S.plan, S.host_inputs, layer_ms):
         d = sp["desc"]
         Oh, Ow = L.Oh, L.Ow
         reps = (d["N"] + xb.shape[0] - 1) // xb.shape[0]
         x_bytes = 4 * d["N"] * d["C"] * d["H"] * d["W"]
         y_bytes = 4 * d["N"] * d["K"] * Oh * Ow
         w_bytes = 4 * d["K"] * d["C"] * d["R"] * d["S"]
+        macs = nze_macs(dict(d, N=xb.shape[0]), xb, Oh, Ow) * reps * (d["N"] / (xb.shape[0] * reps))
+        nnz = int((xb != 0).sum()) * d["N"] / xb.shape[0]
+        enc_bytes = x_bytes + 8 * nnz + 8 * 3 * d["N"] * d["C"]
+        tr_sparse = enc_bytes / (hbm_gbs * 1e9) + max((8 * nnz + w_bytes + y_bytes) / (hbm_gbs * 1e9),
+                                                       2.0 * macs / (p_fp32 * 1e12))
         if algo == "im2col":
             low = 4 * d["N"] * d["C"] * d["R"] * d["S"] * Oh * Ow
             if spc.spc_im2col_engine(d) == spc.SPC_GEMM_TC_3XTF32:
-                # three TF32 products per fp32 MAC at the TF32 tensor peak
-                t_mma = 3 * dense_flops(d, Oh, Ow) / (tf32_peak() * 1e12)
+                t_mma = 3 * dense_flops(d, Oh, Ow) / (tf32_peak() * 1e12)   # three TF32 products per MAC
             else:
                 t_mma = dense_flops(d, Oh, Ow) / (p_fp32 * 1e12)
             tr = max((x_bytes + 2 * low + w_bytes + y_bytes) / (hbm_gbs * 1e9), t_mma)
         else:
-            macs = nze_macs(dict(d, N=xb.shape[0]), xb, Oh, Ow) * reps * (d["N"] / (xb.shape[0] * reps))
-            nnz = int((xb != 0).sum()) * d["N"] / xb.shape[0]
-            enc_bytes = x_bytes + 8 * nnz + 8 * 3 * d["N"] * d["C"]
-            tr = max(enc_bytes / (hbm_gbs * 1e9), 0) + max((8 * nnz + w_bytes + y_bytes) / (hbm_gbs * 1e9),
-                                                          2.0 * macs / (p_fp32 * 1e12))
+            tr = tr_sparse
         t_roof += tr
-        layers.append({"layer": sp["name"], "density": round(sp["density"], 4), "algo": algo})
+        t_roof_sparse += tr_sparse
+        layers.append({"layer": sp["name"], "density": round(sp["density"], 4), "algo": algo,
+                       "device_ms": round(lms, 4), "roofline_frac": round(tr / (lms * 1e-3), 4),
+                       "nze_gflop": round(2.0 * macs / 1e9, 3)})
     res = {"workload": "cfg5 ResNet-50 3x3 stack (16 layers)", "global_batch": args.stack_batch,
-           "per_rank_batch": hi - lo, "n_gpus": world, "mode": args.stack_mode,
+           "per_rank_batch": hi - lo, "n_gpus": world, "mode": mode if not force else f"forced {force}",
+           "plan_source": plan_src,
            "images_per_s": args.stack_batch / (t_tot * 1e-3), "ms_per_step": t_tot, "stack_ms": t_stack,
            "gather_ms": t_gather, "gather": "NCCL all_gather_into_tensor of the last layer's output" if world > 1
            else "none (1 GPU)", "steps": args.stack_steps, "scaling": "strong (global batch fixed)",
@@ -324,24 +519,19 @@ def run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32):
                              "max(compressed + weight + output bytes / HBM, NZE FLOPs / FP32 peak); im2col = "
                              "max(x + 2 x lowered + w + y bytes / HBM, dense FLOPs / FP32 peak (cuBLAS FP32) or "
                              "3 x dense FLOPs / TF32 tensor peak (tcgen05 3xTF32))",
-           "plan": layers, "select_ms_per_sample": S.select_times if rank == 0 else None,
-           "gemm": spc.GEMM_NAMES[spc.spc_get_im2col_gemm()],
+           "plan": layers, "select_ms_per_sample": S.select_times if (rank == 0 and not force) else None,
            "gemm_per_layer": [spc.GEMM_NAMES[spc.spc_im2col_engine(sp["desc"])] for sp in S.specs],
-           "inputs": "8 distinct seeded clustered-ReLU images per layer, tiled to the batch; L2 flushed per step"}
-    if rank == 0 and not args.no_cpu:
-        import oracle
-        oracle.build()
-        t_cpu = 0.0
-        for sp, xb, w in zip(S.specs, S.host_inputs, S.weights):
-            t, n, _ = oracle_time(dict(sp["desc"], N=2), xb[:2], w, budget_s=1e9)
-            t_cpu += t
-        res["cpu_baseline"] = {"value": 2 / t_cpu, "unit": "images/s", "cores": 1, "kind": "oracle",
-                               "sample": "2 images through all 16 layers: oracle CPO encode + Alg. 2 conv, "
-                                         "single thread, FP64"}
-    return res
+           "inputs": "8 distinct seeded clustered-ReLU images per layer, tiled to the batch; every layer's data "
+                     "exceeds L2 at this batch, steps back to back"}
+    if force:
+        res["sparse_roofline_images_per_s"] = (hi - lo) / t_roof_sparse
+    return res, S
 
 
 # ---------------------------------------------------------------- GPU leg
+
+PER_CONFIG = ["cfg1", "cfg2", "cfg3", "cfg3s2", "cfg3@0.05", "cfg3@0.2", "cfg3@0.3", "cfg3@0.5", "cfg4a", "cfg4b"]
+
 
 def run_ours(args):
     import torch
@@ -357,60 +547,26 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+    hbm_gbs, sm_max_mhz, peak_src = load_peaks()
+    p_fp32 = fp32_peak(sm_max_mhz)
 
     c = workload(args.workload)
     d = c["desc"]
-    # each rank draws its own images (weak scaling: independent batches)
-    x = clustered_relu(d["N"], d["C"], d["H"], d["W"], c["density"], c["seed"] + 7919 * rank, c["dead_frac"],
-                       c["zero_tile_frac"])
+    pool = make_pool(c, rank)                       # each rank draws its own images (weak scaling)
     w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
-    from paper_2104_08314_b200.layer import SparseConvLayer
-    Oh, Ow = spc.out_hw(d)
-    xg = torch.from_numpy(x).to(dev)
-    wg = torch.from_numpy(w).to(dev)
-    L_cpo = SparseConvLayer(d, wg, device=dev)
-    L_cps = SparseConvLayer(d, wg, device=dev)
-    y = L_cpo.y
-    enc, enc_s = L_cpo.enc, L_cps.enc
-    flush = torch.empty(int(2 * 128 * 2 ** 20) // 4, dtype=torch.float32, device=dev)  # > 2x L2
+    Oh, Ow = spc_out_hw(d)
+    R = Rotating(d, pool, w, dev)
+    g_step_full = R.graph("step", R.nset)           # capture before the timed region
 
-    # CUDA graphs of each step: the host enqueues a whole step at once, so the
-    # device timeline between the events holds only our kernels.
-    g_cpo = L_cpo.capture(lambda: L_cpo.forward(xg, "cpo"))
-    g_cpo_enc = L_cpo.capture(lambda: L_cpo.encode(xg, "cpo"))
-    g_cpo_conv = L_cpo.capture(lambda: L_cpo.conv())
-    g_cps = L_cps.capture(lambda: L_cps.forward(xg, "cps"))
-    g_cps_enc = L_cps.capture(lambda: L_cps.encode(xg, "cps"))
-    g_i2c = L_cpo.capture(lambda: L_cpo.forward(xg, "im2col"))
-    L_cpo.forward(xg, "cpo")       # leave the CPO encoding in place for the conv-only graph
-
-    step_ms = {}
-
-    def timed(graph, steps, warmup, flush_l2=True, key=None):
-        for _ in range(warmup):
-            graph.replay()
-        torch.cuda.synchronize()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        for i in range(steps):
-            if flush_l2:
-                flush.zero_()                  # L2 flush between timed steps (outside the events)
-            ev[i][0].record(stream)
-            graph.replay()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        ts = [a.elapsed_time(b) for a, b in ev]
-        if key:
-            step_ms[key] = ts
-        return sum(ts)
-
-    # --- main timed region (CPO path), barrier + sync on both sides, max over ranks
-    for _ in range(args.warmup):
-        g_cpo.replay()
+    # --- main timed region (CPO encode + conv), barrier + sync on both sides, max over ranks
+    for _ in range(max(1, args.warmup // R.nset + 1)):
+        g_step_full.replay()
+    R.timed("step", args.warmup, stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        t_ms = timed(g_cpo, args.steps, 0, key="cpo")
+        t_ms = R.timed("step", args.steps, stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -422,104 +578,86 @@ def run_ours(args):
     flops_step = dense_flops(d, Oh, Ow)
     value = flops_step * args.steps * world / (tmax * 1e-3) / 1e9
 
-    # --- per-kernel breakdown and the other algorithms (same process)
-    t_hot_ms = timed(g_cpo, args.steps, 1, flush_l2=False)   # hot L2: no flush
-    t_enc_ms = timed(g_cpo_enc, args.steps, 1)
-    t_conv_ms = timed(g_cpo_conv, args.steps, 1)
-    t_cps = timed(g_cps, args.steps, 1)
-    t_cps_enc = timed(g_cps_enc, args.steps, 1)
-    t_i2c = timed(g_i2c, args.steps, 1)
+    # --- per-launch kernel durations (back to back over the same rotating sets, L2-cold):
+    #     the rooflines use these averages
+    k_steps = max(args.steps, 4 * R.nset)
+    k_enc_ms = R.timed("encode", k_steps, stream) / k_steps
+    k_conv_ms = R.timed("conv", k_steps, stream) / k_steps
+    t_cps_ms = R.timed("cps", args.steps, stream) / args.steps
+    t_i2c_ms = R.timed("im2col", args.steps, stream) / args.steps
 
-    # Per-launch kernel durations for the rooflines: timing events recorded INSIDE a
-    # graph right around the one kernel (external event-record nodes on the stream
-    # the kernel is launched on), an L2 flush before each, so the graph launch and
-    # the event round trip to the host (~6 us per step on this pool) are not in it.
-    def kernel_timed(fn, steps, reps=50):
-        reps = max(1, min(reps, steps))
-        evs = [(torch.cuda.Event(enable_timing=True, external=True),
-                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(reps)]
-
-        def body():
-            for a, b in evs:
-                flush.zero_()
-                a.record()
-                fn()
-                b.record()
-        g = L_cpo.capture(body, warmup=1)
-        ts = []
-        for _ in range(max(1, steps // reps) + 1):   # first replay is warm-up
-            g.replay()
-            torch.cuda.synchronize()
-            ts.append([a.elapsed_time(b) for a, b in evs])
-        ts = [t for row in ts[1:] for t in row]
-        return float(np.mean(ts)), float(np.median(ts))
-
-    k_conv_ms, k_conv_med = kernel_timed(lambda: L_cpo.conv(), args.steps)
-    k_enc_ms, k_enc_med = kernel_timed(lambda: L_cpo.encode(xg, "cpo"), args.steps)
-    L_cpo.forward(xg, "cpo")
-
-    # encoding sizes, CR (paper units: elements of ptr + DA + IN vs S_im2col)
-    pl_, dl_, il_ = spc.spc_encoding_lengths(enc)
-    ps_, ds_, is_ = spc.spc_encoding_lengths(enc_s)
+    L0 = R.layers[0]
+    L0.forward(R.xs[0], "cpo")
+    pl_, dl_, il_ = L0.lengths()
+    L0.forward(R.xs[0], "cps")
+    ps_, ds_, is_ = L0.lengths()
+    L0.forward(R.xs[0], "cpo")
+    x0 = R.xs[0].cpu().numpy()
     s_im2col = d["N"] * Oh * Ow * d["C"] * d["R"] * d["S"]
     side = 3 * (d["N"] * d["C"] + 1) * 2   # int64 side tables in 4-byte elements
     cr_cpo = s_im2col / (pl_ + dl_ + il_)
     cr_cps = s_im2col / (ps_ + ds_ + is_)
 
     # --- roofline of the dominant kernel (measured per-launch averages)
-    hbm_gbs, sm_max_mhz, peak_src = load_peaks()
-    p_fp32 = SM_COUNT * FP32_LANES * 2 * sm_max_mhz * 1e6 / 1e12   # TFLOP/s, derived
-    macs = nze_macs(d, x, Oh, Ow)
-    conv_bytes = 4 * (pl_ + dl_ + il_) + 8 * 2 * (d["N"] * d["C"] + 1) + 4 * wg.numel() + 4 * y.numel()
-    enc_bytes = 4 * xg.numel() + 4 * (pl_ + dl_ + il_) + 8 * 3 * (d["N"] * d["C"] + 1)
-    conv_s = k_conv_ms * 1e-3          # average launch duration (in-graph events)
-    enc_s = k_enc_ms * 1e-3
+    macs = nze_macs(d, x0, Oh, Ow)
+    conv_bytes = 4 * (pl_ + dl_ + il_) + 8 * 2 * (d["N"] * d["C"] + 1) + 4 * w.size + 4 * d["N"] * d["K"] * Oh * Ow
+    enc_bytes = 4 * x0.size + 4 * (pl_ + dl_ + il_) + 8 * 3 * (d["N"] * d["C"] + 1)
+    conv_s, enc_s = k_conv_ms * 1e-3, k_enc_ms * 1e-3
     conv_flops = 2.0 * macs
     t_roof_conv = max(conv_bytes / (hbm_gbs * 1e9), conv_flops / (p_fp32 * 1e12))
     conv_bound = "alu" if conv_flops / (p_fp32 * 1e12) >= conv_bytes / (hbm_gbs * 1e9) else "hbm"
-    traffic = None
+    traffic, traffic_src = None, None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.workload, {}).get("sparse_conv")
+            tj = json.load(open(tfile))
+            traffic = tj.get(args.workload, {}).get("sparse_conv" if conv_s >= enc_s else "encode")
+            traffic_src = tj.get("_source")
         except Exception:
             traffic = None
     if conv_s >= enc_s:
-        if conv_bound == "alu":
-            roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "alu", "achieved": conv_flops / conv_s / 1e12,
-                    "peak": p_fp32, "unit": "TFLOP/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
-                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock",
-                    "algorithmic_flops": conv_flops, "algorithmic_bytes": conv_bytes,
-                    "duration_us": conv_s * 1e6}
-        else:
-            roof = {"kernel": "strip_conv_kernel (sparse conv)", "bound": "hbm", "achieved": conv_bytes / conv_s / 1e9,
-                    "peak": hbm_gbs, "unit": "GB/s", "frac": t_roof_conv / conv_s, "traffic": traffic,
-                    "peak_source": peak_src, "algorithmic_bytes": conv_bytes}
+        roof = {"kernel": "sparse conv (strip_conv_kernel)", "bound": conv_bound,
+                "achieved": conv_flops / conv_s / 1e12 if conv_bound == "alu" else conv_bytes / conv_s / 1e9,
+                "peak": p_fp32 if conv_bound == "alu" else hbm_gbs, "unit": "TFLOP/s" if conv_bound == "alu" else "GB/s",
+                "frac": t_roof_conv / conv_s, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock (tools/ffma_peak.cu measured "
+                               "72.6 TFLOP/s)" if conv_bound == "alu" else peak_src,
+                "algorithmic_flops_per_launch": conv_flops, "algorithmic_bytes_per_launch": conv_bytes,
+                "launch_us": conv_s * 1e6,
+                "timing": f"mean launch duration over {k_steps} back-to-back launches (CUDA events on the "
+                          f"launching stream), {R.l2_note()}"}
     else:
         roof = {"kernel": "encode_kernel", "bound": "hbm", "achieved": enc_bytes / enc_s / 1e9, "peak": hbm_gbs,
-                "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs, "traffic": None,
-                "peak_source": peak_src, "algorithmic_bytes": enc_bytes}
+                "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs, "traffic": traffic,
+                "traffic_source": traffic_src, "peak_source": peak_src, "algorithmic_bytes_per_launch": enc_bytes,
+                "launch_us": enc_s * 1e6}
 
     # --- end to end through the public API with host buffers: pinned H2D of the
     # input, encode + conv, D2H of the output, all inside the timed region
-    xh = torch.from_numpy(x).pin_memory()
+    xg, y = R.xs[0], L0.y
+    xh = torch.from_numpy(x0).pin_memory()
     yh = torch.empty(y.shape, dtype=torch.float32).pin_memory()
 
     def e2e_step():
         xg.copy_(xh, non_blocking=True)
-        L_cpo.forward(xg, "cpo")
+        L0.forward(xg, "cpo")
         yh.copy_(y, non_blocking=True)
-    g_e2e = L_cpo.capture(e2e_step)
-    e2e_serial_ms = timed(g_e2e, args.steps, 2)
+    g_e2e = L0.capture(e2e_step)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        g_e2e.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_serial_ms = e0.elapsed_time(e1)
 
-    # Pipelined form of the same steps (what a serving loop does): two layer instances
-    # with their own input / encoding / output buffers; per step, H2D on one stream,
-    # encode + conv on a second, D2H on a third, so step i's copies overlap the
-    # neighbouring steps' compute.  One graph holds PIPE steps (fill and drain included);
-    # every step still copies its whole input in and its whole output out.
+    # Pipelined form of the same steps (what a serving loop does): two buffer sets; per step,
+    # H2D on one stream, encode + conv on a second, D2H on a third, so step i's copies
+    # overlap the neighbouring steps' compute.  One graph holds PIPE steps.
     PIPE = 16
-    Ls = [L_cpo, SparseConvLayer(d, wg, device=dev)]
-    xgs = [xg, torch.empty_like(xg)]
+    Ls = [R.layers[0], R.layers[1]]
+    xgs = [R.xs[0], R.xs[1]]
     yhs = [yh, torch.empty(y.shape, dtype=torch.float32).pin_memory()]
     s_h, s_c, s_d = (torch.cuda.Stream(device=dev) for _ in range(3))
     ev_h = [torch.cuda.Event() for _ in range(PIPE)]
@@ -556,70 +694,116 @@ def run_ours(args):
     with torch.cuda.graph(g_pipe):
         pipeline()
     reps = max(1, args.steps // PIPE)
-    e2e_ms = timed(g_pipe, reps, 2) * args.steps / (reps * PIPE)   # per-step mean, scaled to K steps
+    e0.record(stream)
+    for _ in range(reps):
+        g_pipe.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) * args.steps / (reps * PIPE)   # per-step mean, scaled to K steps
     if world > 1:
         tt = torch.tensor([e2e_ms, e2e_serial_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms, e2e_serial_ms = float(tt[0].item()), float(tt[1].item())
     e2e_val = flops_step * args.steps * world / (e2e_ms * 1e-3) / 1e9
+    R_note = R.l2_note()
+    del R, g_step_full, g_e2e, g_pipe
+    torch.cuda.empty_cache()
+
+    # --- per-config rows (rank 0 draws them; each row is its own rotating buffer set)
+    rows = []
+    if not args.no_configs:
+        y4a = None
+        for name in PER_CONFIG:
+            base, _, dens = name.partition("@")
+            cc = dict(workload(base))
+            if dens:
+                cc["density"] = float(dens)
+            dd = cc["desc"]
+            if base == "cfg4b":
+                if y4a is None:
+                    continue
+                pool_c = y4a            # ReLU(cfg4a output): the intermediate re-sparsified by ReLU
+            else:
+                pool_c = make_pool(cc, rank)
+            wc = he_normal(dd["K"], dd["C"], dd["R"], dd["S"], cc["seed"] + (1 if base == "cfg4b" else 0))
+            row, Rc = measure_layer(name, dd, pool_c, wc, dev, stream, args.config_steps, hbm_gbs, p_fp32)
+            if base == "cfg4a":
+                L = Rc.layers[0]
+                L.relu = True
+                L.forward(Rc.xs[0], "cpo")
+                y4a = L.y.cpu().numpy()
+                L.relu = False
+            rows.append(row)
+            del Rc
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        t, n, f = oracle_time(d, x, w, budget_s=args.cpu_budget)
+        t, n, f = oracle_time(d, pool[:d["N"]], w, budget_s=args.cpu_budget)
         cpu = {"value": f / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
                "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
                "sample": f"{n} image(s) of {args.workload}: oracle CPO encode + Alg. 2 conv, single thread, FP64"}
-        cpu["legs"] = oracle_legs(d, x, w)
-        t2, n2, f2, thr = oracle_time_threads(d, x, w, args.cpu_budget, os.cpu_count() or 1)
+        cpu["legs"] = oracle_legs(d, pool[:d["N"]], w)
+        t2, n2, f2, thr = oracle_time_threads(d, pool[:d["N"]], w, args.cpu_budget, os.cpu_count() or 1)
         cpu["all_cores"] = {"value": f2 / t2 / 1e9, "unit": "GFLOP/s", "cores": thr,
                             "sample": f"{n2} image(s): encode on one thread, Alg. 2 over {thr} output-channel "
                                       "slices in parallel threads"}
 
-    stack = None
+    stack = stack_cpo = None
     if not args.no_stack:
-        stack = run_stack(args, world, rank, dev, flush, hbm_gbs, p_fp32)
+        stack, S = run_stack(args, world, rank, dev, hbm_gbs, p_fp32, mode=args.stack_mode)
+        stack_cpo, _ = run_stack(args, world, rank, dev, hbm_gbs, p_fp32, force="cpo", S=S)
+        if rank == 0 and not args.no_cpu:
+            import oracle
+            oracle.build()
+            t_cpu = 0.0
+            for sp, xb, wl in zip(S.specs, S.host_inputs, S.weights):
+                t, n, _ = oracle_time(dict(sp["desc"], N=2), xb[:2], wl, budget_s=1e9)
+                t_cpu += t
+            stack["cpu_baseline"] = {"value": 2 / t_cpu, "unit": "images/s", "cores": 1, "kind": "oracle",
+                                     "sample": "2 images through all 16 layers: oracle CPO encode + Alg. 2 conv, "
+                                               "single thread, FP64"}
+        del S
+        torch.cuda.empty_cache()
 
     if world > 1:
         dist.barrier()
     if rank == 0:
-        us = lambda ms: 1e3 * ms / args.steps  # noqa: E731
+        us = lambda ms: 1e3 * ms  # noqa: E731
         line = {
             "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "ms_per_step_median": float(np.median(step_ms["cpo"])) if rank == 0 else None,
+            "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"],
                        "dead_frac": c["dead_frac"], "zero_tile_frac": c["zero_tile_frac"],
-                       "l2": "flushed between timed steps (256 MiB write)", "global_batch": d["N"] * world},
-            "layer_us": {"cpo_encode": us(t_enc_ms), "cpo_conv": us(t_conv_ms), "cpo_total": us(t_ms),
-                         "cpo_total_hot_l2": us(t_hot_ms),
-                         "cps_encode": us(t_cps_enc), "cps_conv": us(t_cps - t_cps_enc), "cps_total": us(t_cps),
-                         "im2col_total": us(t_i2c)},
-            "kernel_us": {"timing": "per launch, timing events inside a graph around the one kernel, L2 flushed before each",
-                          "cpo_conv_mean": 1e3 * k_conv_ms, "cpo_conv_median": 1e3 * k_conv_med,
-                          "cpo_encode_mean": 1e3 * k_enc_ms, "cpo_encode_median": 1e3 * k_enc_med},
-            "im2col": {"value": flops_step * args.steps / (t_i2c * 1e-3) / 1e9, "unit": "GFLOP/s",
+                       "l2": R_note, "global_batch": d["N"] * world},
+            "layer_us": {"cpo_step": us(tmax / args.steps), "cpo_encode": us(k_enc_ms), "cpo_conv": us(k_conv_ms),
+                         "cps_step": us(t_cps_ms), "im2col_step": us(t_i2c_ms)},
+            "kernel_us": {"timing": "mean per launch, back-to-back launches over the rotating L2-cold buffer sets",
+                          "cpo_conv": us(k_conv_ms), "cpo_encode": us(k_enc_ms)},
+            "im2col": {"value": flops_step / (t_i2c_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                        "gemm": spc.GEMM_NAMES[spc.spc_im2col_engine(d)]},
-            "speedup_vs_im2col": t_i2c / t_ms,
+            "speedup_vs_im2col": t_i2c_ms / (tmax / args.steps),
             "cr": {"cpo": cr_cpo, "cps": cr_cps, "cpo_with_side_tables": s_im2col / (pl_ + dl_ + il_ + side),
                    "ptr": pl_, "da": dl_, "in_cpo": il_, "in_cps": is_, "S_im2col": s_im2col},
-            "nze_macs": macs, "density_measured": float((x != 0).mean()),
+            "nze_macs": macs, "density_measured": float((x0 != 0).mean()),
             "roofline": roof,
             "roofline_encode": {"bound": "hbm", "achieved": enc_bytes / enc_s / 1e9, "peak": hbm_gbs,
                                 "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs},
-            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": int(4 * xg.numel()),
-                    "d2h_bytes_per_step": int(4 * y.numel()), "ms_per_step": e2e_ms / args.steps,
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": int(4 * x0.size),
+                    "d2h_bytes_per_step": int(4 * d["N"] * d["K"] * Oh * Ow), "ms_per_step": e2e_ms / args.steps,
                     "form": f"pipelined: H2D / encode+conv / D2H on three streams, {PIPE} steps per graph "
-                            "(fill and drain included), two buffer sets; no L2 flush inside the graph "
-                            "(each step's input arrives from the host)",
+                            "(fill and drain included), two buffer sets",
                     "serial": {"value": flops_step * args.steps * world / (e2e_serial_ms * 1e-3) / 1e9,
                                "ms_per_step": e2e_serial_ms / args.steps,
                                "form": "one step per graph: H2D, encode, conv, D2H in sequence"}},
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "configs": rows,
             "stack": stack,
+            "stack_cpo": stack_cpo,
             "version": spc.spc_version(),
         }
         print(json.dumps(line))
@@ -630,10 +814,13 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config rows")
+    ap.add_argument("--config-steps", type=int, default=200)
+    ap.add_argument("--plan-file", default="", help="read the cfg5 plan from this file (skip selection)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stack", action="store_true", help="skip the cfg5 stack leg")

@@ -398,11 +398,9 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
             a.lengths[0] = t0;
             a.lengths[1] = t1;
             a.lengths[2] = t2;
-            // bit 0: capacity overflow of this launch; bits 1-2 (wait timeouts) are sticky
-            unsigned long long* ov = reinterpret_cast<unsigned long long*>(a.lengths + 3);
-            const unsigned long long o = (t0 > a.cap_ptr || t1 > a.cap_da || t2 > a.cap_in) ? 1ull : 0ull;
-            atomicAnd(ov, ~1ull);
-            if (o) atomicOr(ov, o);
+            // the whole word: bit 0 = capacity overflow of this launch (a launch that completes
+            // here had every predecessor publish, so no wait of it timed out)
+            a.lengths[3] = (t0 > a.cap_ptr || t1 > a.cap_da || t2 > a.cap_in) ? 1 : 0;
             a.st->count[(s_epoch + 1u) & 1u] = 0;   // the next launch's counter (unused in this one)
             a.st->epoch = s_epoch + 1u;
         }

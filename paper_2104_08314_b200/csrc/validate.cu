@@ -144,7 +144,6 @@ __global__ void validate_kernel(Geom g, const int32_t* __restrict__ ptr, const f
             // (k = 1, 2) or {first index, pattern} (k >= 3); decoded count == block count
             int lo = 0, e = 0;
             for (int s = 0; s <= Ow1 - g.S; s++) {
-                const int w = s + g.S - 1;
                 const int want = c[s] - lo;
                 int got = 0, prev_row = -1;
                 while (got < want) {

@@ -65,6 +65,32 @@ def gather_outputs(y: torch.Tensor, n_per_rank: list[int]) -> torch.Tensor:
     return torch.cat([p[:n] for p, n in zip(parts, n_per_rank)])
 
 
+def save_plan(path: str, layers: list[str], plan: list[str], mode: str, times_ms=None, density=None) -> None:
+    """Persist a per-layer plan (the offline selection's result) so that ranks
+    read it instead of re-selecting: written atomically (tmp + rename)."""
+    import os
+    doc = {"format": "spconv-b200 plan v1", "mode": mode, "layers": list(layers), "plan": list(plan),
+           "select_times_ms": times_ms, "density": density}
+    tmp = f"{path}.tmp{os.getpid()}"
+    with open(tmp, "w") as f:
+        json.dump(doc, f)
+    os.replace(tmp, path)
+
+
+def load_plan(path: str, layers: list[str] | None = None) -> list[str]:
+    """Read a plan file written by save_plan; checks the layer names when given."""
+    with open(path) as f:
+        doc = json.load(f)
+    if doc.get("format") != "spconv-b200 plan v1":
+        raise ValueError(f"{path}: not a plan file")
+    if layers is not None and list(doc["layers"]) != list(layers):
+        raise ValueError(f"{path}: plan is for layers {doc['layers']}")
+    plan = list(doc["plan"])
+    if any(a not in ALGOS for a in plan):
+        raise ValueError(f"{path}: bad algorithm in {plan}")
+    return plan
+
+
 def tile_images(base: np.ndarray, n: int) -> np.ndarray:
     """Fill a batch of n images by repeating `base` [b, C, H, W] (b distinct seeded
     images per layer; DESIGN.md §4 input recipe for the cfg5 stack)."""
@@ -134,6 +160,16 @@ class Cfg5Stack:
 
     def capture(self) -> torch.cuda.CUDAGraph:
         return self.layers[0].capture(self.forward)
+
+    def replay(self, times_ms: list[list[float]], mode: str = "best_of_three") -> list[str]:
+        """The plan from RECORDED per-layer times {im2col, CPO, CPS} (SPEC.md:741 replay):
+        the same argmin / tie rule as select_layer_algo, through the C ABI, no GPU work."""
+        if len(times_ms) != len(self.layers):
+            raise ValueError("one time triple per layer")
+        plan = [B.ALGO_NAMES[B.spc_select_from_times(t, L.sparse_ok and t[1] >= 0 and t[2] >= 0, MODES[mode])]
+                for t, L in zip(times_ms, self.layers)]
+        self.plan, self.select_times = plan, [list(map(float, t)) for t in times_ms]
+        return plan
 
     def plan_json(self) -> str:
         return json.dumps({"layers": [sp["name"] for sp in self.specs], "plan": self.plan,

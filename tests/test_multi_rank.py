@@ -64,3 +64,40 @@ def test_gloo_world2_plan_and_gather(n):
         assert plan == ["cpo", "im2col", "cps"]
         assert tuple(shape) == (n, 3, 2, 2)
         assert np.array_equal(vals, np.arange(n))
+
+
+def _plan_worker(rank, world, port, path, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2104_08314_b200.stack import load_plan, save_plan
+        names = [f"L{i:02d}" for i in range(16)]
+        if rank == 0:   # the offline selection runs once, on rank 0, and persists the plan
+            save_plan(path, names, ["im2col"] * 8 + ["cpo"] * 4 + ["cps"] * 4, "best_of_three",
+                      times_ms=[[1.0, 2.0, 3.0]] * 16)
+        dist.barrier()  # control plane only; the plan itself travels through the file
+        q.put((rank, load_plan(path, names)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_plan_file(tmp_path):
+    """the per-layer plan is computed once (rank 0) and READ FROM A PLAN FILE
+    by every rank -- no collective carries it."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    path = str(tmp_path / "plan.json")
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, 2, port, path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = ["im2col"] * 8 + ["cpo"] * 4 + ["cps"] * 4
+    assert all(plan == want for _, plan in res)
+    from paper_2104_08314_b200.stack import load_plan
+    with pytest.raises(ValueError):
+        load_plan(path, [f"X{i}" for i in range(16)])
