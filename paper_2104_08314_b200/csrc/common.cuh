@@ -142,8 +142,19 @@ __device__ __forceinline__ void probe(int slot) {
         g_probe[b][slot][1] = clock64();
     }
 }
+// any thread may stamp (the caller elects it)
+__device__ __forceinline__ void probe_any(int slot) {
+    if (blockIdx.x + blockIdx.y * gridDim.x + blockIdx.z * gridDim.x * gridDim.y < kProbeCtas && slot < kProbeSlots) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const unsigned b = blockIdx.x + blockIdx.y * gridDim.x + blockIdx.z * gridDim.x * gridDim.y;
+        g_probe[b][slot][0] = t;
+        g_probe[b][slot][1] = clock64();
+    }
+}
 #else
 __device__ __forceinline__ void probe(int) {}
+__device__ __forceinline__ void probe_any(int) {}
 #endif
 
 // Programmatic dependent launch (sm_90+): a secondary kernel launched with

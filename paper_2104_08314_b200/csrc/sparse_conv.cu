@@ -1386,10 +1386,23 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
     return cudaErrorNotSupported;
 }
 
+#include "ws_conv.cuh"
+
+static bool conv_v1_forced() {   // development A/B: SPC_CONV_V1=1 runs the round-1 strip kernel
+    static const char* env = getenv("SPC_CONV_V1");
+    return env && atoi(env) != 0;
+}
+
 size_t conv_scratch_bytes(const Geom& g) {
     size_t bytes = 0;
     visit_strip_cfg(g, [&](auto cfg) {
         bytes = plan_strip<decltype(cfg)>(g).scratch_bytes;
+        return cudaSuccess;
+    });
+    const int pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
+    visit_ws_cfg(g, [&](auto cfg) {
+        WsPlan<decltype(cfg)> p;
+        if (plan_ws<decltype(cfg)>(g, pmax, p)) bytes = std::max(bytes, p.scratch_bytes);
         return cudaSuccess;
     });
     return bytes ? kSkFlagBytes + bytes : 0;
@@ -1426,7 +1439,10 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         a.scratch_bytes = scratch_bytes - kSkFlagBytes;
     }
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
-    cudaError_t err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
+    cudaError_t err = cudaErrorNotSupported;
+    if (!conv_v1_forced()) err = visit_ws_cfg(g, [&](auto cfg) { return run_ws<decltype(cfg)>(a, st); });
+    if (err != cudaErrorNotSupported) return err;
+    err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;

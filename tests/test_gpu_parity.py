@@ -413,3 +413,28 @@ def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
     finally:
         spc.spc_set_im2col_gemm(prev)
     _check_conv(got, ref, f"tc 3xtf32 {shape}")
+
+
+# ------------------------------------------------ warp-specialised conv (v2) configurations
+
+@pytest.mark.parametrize("shape", [
+    (2, 40, 14, 14, 256, 1),     # 14x14 @ 256, s1: 2x4 tiles x 4 channels per lane, cluster split
+    (3, 24, 7, 7, 512, 1),       # 7x7 @ 512, s1: 4x4 tiles x 2 channels per lane, 8 k-groups
+    (2, 20, 14, 14, 512, 2),     # 14 -> 7 @ 512, s2
+    (2, 36, 28, 28, 256, 2),     # 28 -> 14 @ 256, s2
+    (1, 300, 14, 14, 256, 1),    # many chunks (NST-stage ring wraps several times), ragged last chunk
+])
+@pytest.mark.parametrize("rho", [0.0, 0.07, 0.4, 1.0])
+def test_ws_conv_integer_exact(oracle_mod, shape, rho):
+    """The warp-specialised conv (ws_conv.cuh) against the oracle's Eq. 1 on integer data:
+    every output element exactly equal (ragged chunks, all-zero and dense maps, cluster split)."""
+    N, C, H, W, K, s = shape
+    d = layer_desc(N, C, H, W, K, 3, 3, s, s, 1, 1, 1, 1)
+    x = int_map(N, C, H, W, rho, 1000 + C)
+    x[:, ::7] = 0                                   # some NPC channels
+    w = int_weights(K, C, 3, 3, 7)
+    L = GpuLayer(d, w)
+    L.encode(torch.from_numpy(x).cuda())
+    y = L.conv().cpu().numpy()
+    ref = oracle_mod.direct_conv(d, x, w)
+    assert np.array_equal(y, ref.astype(np.float32)), np.abs(y - ref).max()
