@@ -16,6 +16,9 @@ accumulation), which follows the paper step by step:
   sparse_conv        Alg. 2 / Alg. 4 / SI Alg. 6
   set4_census        C'_k, C''_k of SI Eq. 5
   mac_count          exact multiply-adds of the sparse conv reading A27
+  cscc_encode        CSCC (SI Alg. 5 for any K_w, s_w)
+  cscc_conv          CSCC conv (SI Alg. 6 + stride)
+  cscc_decode        inverse of the CSCC streams            (test of the encoder)
 
 Sizes (SI Eqs. 2-6, 11) are written out in ``sizes.py``.
 
@@ -36,7 +39,7 @@ import subprocess
 import numpy as np
 
 from .sizes import (S_im2col, S_mec, ptr_size_eq3, in_cps_size_eq5, op_size_eq2,  # noqa: F401
-                    nop_size, da_size_eq4)
+                    nop_size, da_size_eq4, S_cscc_eq17, rho_hat, p_bound_cscc, q_bound_cscc)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
@@ -83,6 +86,9 @@ def _L():
             "oc_set4_census": (None, [P, vp, vp]),
             "oc_count_flags": (None, [vp, i64, vp, vp]),
             "oc_pattern_size": (i32, [i32]), "oc_next_offset": (i32, [i32, i32]),
+            "oc_cscc_encode": (ctypes.c_int, [P, vp, vp, i64, vp, i64, vp, i64, vp, vp]),
+            "oc_cscc_conv": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp, vp]),
+            "oc_cscc_decode": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -233,3 +239,46 @@ def pattern_size(p: int) -> int:
 
 def next_offset(p: int, g: int) -> int:
     return int(_L().oc_next_offset(p, g))
+
+
+def cscc_encode(d: dict, x: np.ndarray) -> Encoding:
+    """CSCC streams (SI Alg. 5 for any K_w and s_w; Eq. 17 layout)."""
+    x = _f32(x)
+    NC = d["N"] * d["C"]
+    _, Ow = out_hw(d)
+    cap_ptr = NC * (Ow + 1)
+    cap_da = max(1, NC * Ow * d["S"] * (d["H"] + d["pad_top"] + d["pad_bottom"]))
+    ptr = np.empty(cap_ptr, dtype=np.int32)
+    da = np.empty(cap_da, dtype=np.float32)
+    inn = np.empty(cap_da, dtype=np.int32)
+    off = np.empty(3 * (NC + 1), dtype=np.int64)
+    lens = np.zeros(3, dtype=np.int64)
+    rc = _L().oc_cscc_encode(ctypes.byref(_desc(d)), _p(x), _p(ptr), cap_ptr, _p(da), cap_da, _p(inn), cap_da,
+                             _p(off), _p(lens))
+    if rc != 0:
+        raise RuntimeError(f"oracle cscc overflow, needed {lens.tolist()}")
+    off = off.reshape(3, NC + 1)
+    return Encoding(ptr=ptr[:lens[0]].copy(), da=da[:lens[1]].copy(), inn=inn[:lens[2]].copy(),
+                    chan_ptr_off=off[0].copy(), chan_nz_off=off[1].copy(), chan_in_off=off[2].copy(),
+                    cps=False, cscc=True)
+
+
+def cscc_conv(d: dict, enc: Encoding, w: np.ndarray) -> np.ndarray:
+    """SI Alg. 6 over CSCC streams, FP64 -> [N, K, Oh, Ow]."""
+    Oh, Ow = out_hw(d)
+    y = np.empty((d["N"], d["K"], Oh, Ow), dtype=np.float64)
+    ptr, da = enc["ptr"], enc["da"]
+    rc = _L().oc_cscc_conv(ctypes.byref(_desc(d)), _p(ptr), ptr.size, _p(da), da.size, _p(enc["inn"]),
+                           _p(_f32(w)), _p(y))
+    if rc != 0:
+        raise ValueError("corrupt CSCC streams")
+    return y
+
+
+def cscc_decode(d: dict, enc: Encoding) -> np.ndarray:
+    x = np.empty((d["N"], d["C"], d["H"], d["W"]), dtype=np.float32)
+    ptr, da = enc["ptr"], enc["da"]
+    rc = _L().oc_cscc_decode(ctypes.byref(_desc(d)), _p(ptr), ptr.size, _p(da), da.size, _p(enc["inn"]), _p(x))
+    if rc != 0:
+        raise ValueError("corrupt CSCC streams")
+    return x

@@ -592,3 +592,120 @@ void oc_count_flags(const int32_t *ptr, int64_t n_ptr, int64_t *npf, int64_t *np
         if (ptr[i] == OC_NPC) (*npc)++;
     }
 }
+
+/* ------------------------------------------------- CSCC (the paper's comparison method) */
+
+/* CSCC encoding (fan2019cscc, as simplified by SI Alg. 5, which the
+ * paper says is "designed for any value of K_w and s_w"): every output
+ * column s (stride s_w) owns the K_w-wide submatrix of padded columns
+ * [s*s_w, s*s_w + K_w) -- the lowered matrix LM of SI Eq. 17 -- and
+ * its NZEs are stored row-major inside the submatrix (Alg. 5 lines 10-27: w runs to
+ * s + K_w - 1, then h++), IN = (w - s*s_w) + h*K_w, with ptr = [0, c_0 .. c_{O_w-1}]
+ * channel-cumulative counts per submatrix (O_w + 1 entries per channel; CSCC has no
+ * NPC flag: Eq. 17 charges every channel O_w + 1).  Padded frame (reading A30).
+ * chan_off (optional, [3][N*C+1]) and lens as oc_encode.  Returns 0 or -1 (capacity). */
+int oc_cscc_encode(const oc_desc *d, const float *x, int32_t *ptr, int64_t cap_ptr, float *da, int64_t cap_da,
+                   int32_t *in, int64_t cap_in, int64_t *chan_off, int64_t *lens)
+{
+    int32_t Hp = d->H + d->pt + d->pb, Ow = oc_out_w(d), K_w = d->S;
+    int64_t np = 0, nz = 0, NC = (int64_t)d->N * d->C;
+    int overflow = 0;
+    for (int32_t n = 0; n < d->N; n++)
+        for (int32_t c = 0; c < d->C; c++) {
+            int64_t j = (int64_t)n * d->C + c;
+            if (chan_off) { chan_off[j] = np; chan_off[NC + 1 + j] = nz; chan_off[2 * (NC + 1) + j] = nz; }
+            const float *pl = plane_of(x, d, n, c);
+            int32_t nz_ptr = 0;
+            if (np < cap_ptr) ptr[np] = 0; else overflow = 1;
+            np++;
+            for (int32_t s = 0; s < Ow; s++) {                 /* one submatrix per output column */
+                for (int32_t h = 0; h < Hp; h++)
+                    for (int32_t w = s * d->sw; w < s * d->sw + K_w; w++) {
+                        float v = I_at(pl, d, h, w);
+                        if (v != 0.0f) {
+                            if (nz < cap_da && nz < cap_in) { da[nz] = v; in[nz] = (w - s * d->sw) + h * K_w; }
+                            else overflow = 1;
+                            nz++;
+                            nz_ptr++;
+                        }
+                    }
+                if (np < cap_ptr) ptr[np] = nz_ptr; else overflow = 1;
+                np++;
+            }
+        }
+    if (chan_off) { chan_off[NC] = np; chan_off[NC + 1 + NC] = nz; chan_off[2 * (NC + 1) + NC] = nz; }
+    lens[0] = np; lens[1] = nz; lens[2] = nz;
+    return overflow ? -1 : 0;
+}
+
+/* CSCC convolution (SI Alg. 6, with the stride of SI Eq. 17's
+ * submatrices): the NZE DA[x] with index `index` of submatrix s contributes, for every
+ * kernel row l, to output row y = index/K_w - l of output column s with tap
+ * t = index%K_w + l*K_w (Alg. 6 lines 1-9); a vertical stride keeps y on the grid
+ * (reading A15).  No NPC skip (CSCC).  y is NKHW in FP64.  Returns 0 or -1. */
+int oc_cscc_conv(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const float *da, int64_t n_da,
+                 const int32_t *in, const float *w, double *y)
+{
+    int32_t Hp = d->H + d->pt + d->pb, Oh1 = Hp - d->R + 1, Oh = oc_out_h(d), Ow = oc_out_w(d), K_w = d->S;
+    memset(y, 0, sizeof(double) * (size_t)d->N * d->K * Oh * Ow);
+    for (int32_t k = 0; k < d->K; k++) {
+        int64_t p = 0, z = 0;
+        for (int32_t n = 0; n < d->N; n++) {
+            double *O = y + ((size_t)n * d->K + k) * Oh * Ow;
+            for (int32_t c = 0; c < d->C; c++) {
+                const float *wkc = w + ((size_t)k * d->C + c) * d->R * d->S;
+                if (p + Ow >= n_ptr || ptr[p] != 0) return -1;
+                int32_t x = 0;                                   /* x = ptr[ptr_sh] (Alg. 6 line 16) */
+                for (int32_t s = 0; s < Ow; s++) {
+                    int32_t end = ptr[p + 1 + s];
+                    if (end < x || z + end > n_da) return -1;
+                    for (int32_t tx = x; tx < end; tx++) {       /* convSpMv(K_h, K_w, O_h, tx, s, IN[tx]) */
+                        int32_t index = in[z + tx];
+                        for (int32_t l = 0; l < d->R; l++) {
+                            int32_t yy = index / K_w - l;
+                            int32_t t = index % K_w + l * K_w;
+                            if (yy >= 0 && yy < Oh1 && yy % d->sh == 0 && yy / d->sh < Oh)
+                                O[(size_t)(yy / d->sh) * Ow + s] += (double)da[z + tx] * (double)wkc[t];
+                        }
+                    }
+                    x = end;
+                }
+                z += x;
+                p += 1 + Ow;
+            }
+        }
+        if (p != n_ptr || z != n_da) return -1;
+    }
+    return 0;
+}
+
+/* Independent inverse of the CSCC streams: every copy of an NZE (one per submatrix that
+ * holds its column) is written back to (h, s*s_w + index%K_w); copies must agree.
+ * Columns no submatrix covers stay 0.  Returns 0 or -1 on inconsistency. */
+int oc_cscc_decode(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const float *da, int64_t n_da,
+                   const int32_t *in, float *x)
+{
+    int32_t Ow = oc_out_w(d), K_w = d->S;
+    int64_t p = 0, z = 0;
+    memset(x, 0, sizeof(float) * (size_t)d->N * d->C * d->H * d->W);
+    for (int32_t n = 0; n < d->N; n++)
+        for (int32_t c = 0; c < d->C; c++) {
+            if (p + Ow >= n_ptr + 1 || ptr[p] != 0) return -1;
+            int32_t prev = 0;
+            for (int32_t s = 0; s < Ow; s++) {
+                int32_t end = ptr[p + 1 + s];
+                if (end < prev || z + end > n_da) return -1;
+                for (int32_t tx = prev; tx < end; tx++) {
+                    int32_t e = in[z + tx], h = e / K_w - d->pt, ww = s * d->sw + e % K_w - d->pl;
+                    if (e < 0 || h < 0 || h >= d->H || ww < 0 || ww >= d->W) return -1;
+                    float *dst = &x[(((size_t)n * d->C + c) * d->H + h) * d->W + ww];
+                    if (*dst != 0.0f && *dst != da[z + tx]) return -1;
+                    *dst = da[z + tx];
+                }
+                prev = end;
+            }
+            z += prev;
+            p += 1 + Ow;
+        }
+    return (p == n_ptr && z == n_da) ? 0 : -1;
+}

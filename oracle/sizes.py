@@ -116,3 +116,58 @@ def s_cpo_worst(d: dict, rho_bar: float) -> float:
     I_n I_c (3 + (ceil(K_w/s_w) - 1)(1 + O_w)) + 2 I_h I_w sum rho."""
     ow = _ow1(d)
     return d["N"] * d["C"] * (3 + (_kw_ceil(d) - 1) * (1 + ow)) + 2 * d["H"] * d["W"] * d["N"] * d["C"] * rho_bar
+
+
+# ---- CSCC (SI §1.3, PAPER.md:643-689) ------------------------------------------------
+#
+# Reading A30 (DESIGN.md): CSCC lowers the PADDED map (like MEC, S2), one K_w-wide
+# submatrix per output column at stride s_w, so I_h = Hp and O_w = the real output width.
+# Reading A31: as A29, the printed P / Q bounds are taken on averages: rho_bar = average
+# channel density, rho_hat_bar = average (over images) lowered-matrix density.
+
+def _ow(d: dict) -> int:
+    return _out(d["W"], d["pad_left"], d["pad_right"], d["S"], d["stride_w"])
+
+
+def rho_hat(d: dict, lowered_nnz: int) -> float:
+    """rho_hat = sum_i rho_hat_i: the lowered-matrix densities of the
+    batch, each over O_w K_w I_h I_c elements."""
+    Hp = d["H"] + d["pad_top"] + d["pad_bottom"]
+    return lowered_nnz / float(_ow(d) * d["S"] * Hp * d["C"])
+
+
+def S_cscc_eq17(d: dict, rho_hat_sum: float) -> float:
+    """SI Eq. 17: I_n I_c (O_w + 1) + 2 O_w K_w I_h I_c rho_hat."""
+    Hp = d["H"] + d["pad_top"] + d["pad_bottom"]
+    ow = _ow(d)
+    return d["N"] * d["C"] * (ow + 1) + 2.0 * ow * d["S"] * Hp * d["C"] * rho_hat_sum
+
+
+def _kc(d: dict) -> int:
+    return -(-d["S"] // d["stride_w"])          # ceil(K_w / s_w)
+
+
+def p_bound_cscc(d: dict, rho_hat_bar: float) -> float:
+    """Average channel density below which S_CPO (worst case) <= S_CSCC:
+    rho_bar <= (2 O_w K_w Hp rho_hat_bar + (O_w + 1)(2 - ceil(K_w/s_w)) - 3) / (2 H W),
+    clipped to [0, 1] (reading A31: the printed bound divided by I_n I_c; the CPO DA / IN
+    term counts the H x W map's NZEs, the lowered matrix the padded Hp rows, reading A30)."""
+    Hp = d["H"] + d["pad_top"] + d["pad_bottom"]
+    ow, kc = _ow(d), _kc(d)
+    b = (2.0 * ow * d["S"] * Hp * rho_hat_bar + (ow + 1) * (2 - kc) - 3) / (2.0 * d["H"] * d["W"])
+    return min(1.0, max(0.0, b))
+
+
+def q_bound_cscc(d: dict) -> float:
+    """Q(rho_hat): the least average lowered-matrix density for which the
+    P bound above is non-negative: (3 - (O_w + 1)(2 - ceil(K_w/s_w))) / (2 O_w I_h K_w)."""
+    Hp = d["H"] + d["pad_top"] + d["pad_bottom"]
+    ow, kc = _ow(d), _kc(d)
+    return (3.0 - (ow + 1) * (2 - kc)) / (2.0 * ow * Hp * d["S"])
+
+
+def s_cpo_worst_kc(d: dict, rho_bar: float) -> float:
+    """Worst-case CPO size of the CSCC derivation with ceil(K_w/s_w):
+    I_n I_c (3 + (kc - 1)(1 + O_w)) + 2 H W I_n I_c rho_bar."""
+    ow, kc = _ow(d), _kc(d)
+    return d["N"] * d["C"] * (3 + (kc - 1) * (1 + ow)) + 2.0 * d["H"] * d["W"] * d["N"] * d["C"] * rho_bar
