@@ -47,7 +47,8 @@ typedef enum {
     SPC_ECORRUPT = -5       /* an encoding failed validation */
 } spc_status;
 
-typedef enum { SPC_ALGO_IM2COL = 0, SPC_ALGO_CPO = 1, SPC_ALGO_CPS = 2 } spc_algo;
+typedef enum { SPC_ALGO_IM2COL = 0, SPC_ALGO_CPO = 1, SPC_ALGO_CPS = 2,
+               SPC_ALGO_CSCC = 3 /* the paper's comparison baseline (cscc_encode), never selected */ } spc_algo;
 
 /* Hybrid selection modes: favour time = argmin{im2col, CPO};
  * favour space = argmin{im2col, CPS}; best of three = argmin over all three. */
@@ -143,6 +144,26 @@ spc_status spc_pack_weights(const spc_conv_desc *d, const float *w_kcrs, float *
  * launch reduces its partial sums through L2 instead of distributed shared memory). */
 spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
                                float *y, int32_t fuse_relu, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- CSCC, the paper's comparison method.
+ * Encoding = SI Alg. 5, the paper's simplification of the CSCC encoder
+ * "designed for any value of K_w and s_w": output column s (stride s_w) owns
+ * the K_w-wide submatrix of padded columns [s*s_w, s*s_w+K_w) -- the lowered matrix of SI
+ * Eq. 17; its NZEs are stored row-major in the submatrix with
+ * IN = (w - s*s_w) + h*K_w (h padded), ptr = [0, c_0 .. c_{O_w-1}] channel-cumulative
+ * (O_w + 1 entries per channel; no NPC flag).  Channels n-major then c; the side tables and
+ * `lengths` as for CPO (algo = SPC_ALGO_CSCC).  Any R, S, stride and padding. */
+/* Host: capacities (ptr = N*C*(O_w+1); da = in = N*C*H*W*ceil(K_w/s_w)). */
+spc_status spc_cscc_capacity(const spc_conv_desc *d, int64_t *ptr_cap, int64_t *da_cap, int64_t *in_cap);
+/* Three launches (per-plane counts, one-CTA scan, per-plane writes); lengths[3] = 1 (and
+ * nothing written) when a capacity is too small.  SPC_EUNSUPPORTED: plane (H*W*4 plus the
+ * per-row counts) larger than one CTA's shared memory. */
+spc_status cscc_encode(const spc_conv_desc *d, const float *x, spc_encoding *out, void *stream);
+/* SI Alg. 6 over a CSCC encoding with packed [C][R][S][K] weights
+ * (spc_pack_weights): y = conv(x, w) in fp32 (NKHW), ReLU if fuse_relu.  A flagged encoding
+ * (lengths[3] != 0) gives y = 0. */
+spc_status cscc_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed, float *y,
+                             int32_t fuse_relu, void *stream);
 
 /* Dense baseline: im2col lowering of x into ws_lowered (SI Eq. 6
  * elements, fp32), then y[n] = W[K x CRS] * L[n].  Layout: [N][C*R*S][Oh*Ow] for the

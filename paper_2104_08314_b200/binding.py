@@ -23,11 +23,11 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 SPC_OK, SPC_EINVAL, SPC_EUNSUPPORTED, SPC_ECAPACITY, SPC_ECUDA, SPC_ECORRUPT = 0, -1, -2, -3, -4, -5
-SPC_ALGO_IM2COL, SPC_ALGO_CPO, SPC_ALGO_CPS = 0, 1, 2
+SPC_ALGO_IM2COL, SPC_ALGO_CPO, SPC_ALGO_CPS, SPC_ALGO_CSCC = 0, 1, 2, 3
 SPC_FAVOUR_TIME, SPC_FAVOUR_SPACE, SPC_BEST_OF_THREE = 0, 1, 2
 SPC_NPC = -(2 ** 31)
 SPC_NPF = -(2 ** 31) + 1
-ALGO_NAMES = {0: "im2col", 1: "cpo", 2: "cps"}
+ALGO_NAMES = {0: "im2col", 1: "cpo", 2: "cps", 3: "cscc"}
 
 
 class SpcError(RuntimeError):
@@ -70,6 +70,9 @@ _sigs = {
     "spc_validate_encoding": [_D, _E, _vp, _sz, _vp],
     "spc_select_from_times": [ctypes.POINTER(ctypes.c_float), _i32, _i32, ctypes.POINTER(_i32)],
     "spc_output_dims": [_D, ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
+    "spc_cscc_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "cscc_encode": [_D, _vp, _E, _vp],
+    "cscc_conv_forward": [_D, _E, _vp, _vp, _i32, _vp],
 }
 for _n, _a in _sigs.items():
     getattr(_lib, _n).argtypes = _a
@@ -284,3 +287,33 @@ def spc_encoding_lengths(enc: Encoding, stream=None) -> tuple[int, int, int]:
 
 def spc_version() -> str:
     return _lib.spc_version().decode()
+
+
+def spc_cscc_capacity(d: dict) -> tuple[int, int, int]:
+    p, a, i = _i64(), _i64(), _i64()
+    _check(_lib.spc_cscc_capacity(ctypes.byref(make_desc(d)), ctypes.byref(p), ctypes.byref(a), ctypes.byref(i)),
+           "spc_cscc_capacity")
+    return p.value, a.value, i.value
+
+
+def alloc_cscc_encoding(d: dict, device="cuda", caps: tuple[int, int, int] | None = None) -> Encoding:
+    pc, dc, ic = caps if caps is not None else spc_cscc_capacity(d)
+    nc1 = d["N"] * d["C"] + 1
+    return Encoding(
+        ptr=torch.empty(max(pc, 1), dtype=torch.int32, device=device),
+        da=torch.empty(max(dc, 1), dtype=torch.float32, device=device),
+        inn=torch.empty(max(ic, 1), dtype=torch.int32, device=device),
+        chan_ptr_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        chan_nz_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        chan_in_off=torch.empty(nc1, dtype=torch.int64, device=device),
+        lengths=torch.zeros(4, dtype=torch.int64, device=device))
+
+
+def cscc_encode(d: dict, x: torch.Tensor, enc: Encoding, stream=None):
+    _check(_lib.cscc_encode(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _stream(stream)), "cscc_encode")
+
+
+def cscc_conv_forward(d: dict, enc: Encoding, w_packed: torch.Tensor, y: torch.Tensor, fuse_relu: bool = False,
+                      stream=None):
+    _check(_lib.cscc_conv_forward(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(w_packed), _ptr(y),
+                                  int(fuse_relu), _stream(stream)), "cscc_conv_forward")

@@ -10,6 +10,10 @@
 namespace spc {
 size_t enc_smem_bytes(const Geom& g);
 const char* validate_reason(int code);
+size_t cscc_smem_bytes(const Geom& g);
+cudaError_t launch_cscc_encode(const Geom& g, const float* x, spc_encoding* e, cudaStream_t st);
+cudaError_t launch_cscc_conv(const Geom& g, const spc_encoding* e, const float* w_packed, float* y, int relu,
+                             cudaStream_t st);
 cudaError_t launch_validate(const Geom& g, const spc_encoding* e, void* rec_dev, cudaStream_t st,
                             long long* bad_channel, int* code);
 }
@@ -154,6 +158,7 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
     spc_status s = check_sparse_geometry(d);
     if (s != SPC_OK) return s;
     if (!enc || !w_packed || !y) return fail(SPC_EINVAL, "null pointer");
+    if (enc->algo != SPC_ALGO_CPO && enc->algo != SPC_ALGO_CPS) return fail(SPC_EINVAL, "not a CPO / CPS encoding");
     const spc_conv_desc& e = enc->geom;
     if (e.N != d->N || e.C != d->C || e.H != d->H || e.W != d->W || e.R != d->R || e.S != d->S ||
         e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom || e.pad_left != d->pad_left ||
@@ -243,6 +248,7 @@ spc_status spc_validate_encoding(const spc_conv_desc* d, const spc_encoding* enc
     spc_status s = check_sparse_geometry(d);
     if (s != SPC_OK) return s;
     if (!enc || !scratch || scratch_bytes < 16) return fail(SPC_EINVAL, "bad argument");
+    if (enc->algo != SPC_ALGO_CPO && enc->algo != SPC_ALGO_CPS) return fail(SPC_EINVAL, "the validator checks CPO / CPS");
     if (!enc->ptr || !enc->da || !enc->in || !enc->chan_ptr_off || !enc->chan_nz_off || !enc->chan_in_off ||
         !enc->lengths)
         return fail(SPC_EINVAL, "null stream pointer in spc_encoding");
@@ -263,6 +269,59 @@ spc_status spc_validate_encoding(const spc_conv_desc* d, const spc_encoding* enc
         return fail(SPC_ECORRUPT, "encoding corrupt at channel segment %lld (n=%lld, c=%lld): %s", bad, bad / g.C,
                     bad % g.C, spc::validate_reason(code));
     return SPC_OK;
+}
+
+// ------------------------------------------------------------ CSCC baseline
+
+namespace {
+spc_status check_cscc_geometry(const spc_conv_desc* d) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    const spc::Geom g = spc::make_geom(*d);
+    if (spc::cscc_smem_bytes(g) > 227 * 1024) return fail(SPC_EUNSUPPORTED, "CSCC: plane too large for one CTA");
+    if ((size_t)4 * g.Oh * 32 * 8 > 227 * 1024) return fail(SPC_EUNSUPPORTED, "CSCC: output too tall");
+    if ((long long)(d->S - 1) + (long long)(g.Hp - 1) * d->S >= (1ll << 31)) return fail(SPC_EUNSUPPORTED, "index overflow");
+    return SPC_OK;
+}
+}  // namespace
+
+spc_status spc_cscc_capacity(const spc_conv_desc* d, int64_t* ptr_cap, int64_t* da_cap, int64_t* in_cap) {
+    spc_status s = check_cscc_geometry(d);
+    if (s != SPC_OK) return s;
+    const spc::Geom g = spc::make_geom(*d);
+    // an NZE is stored once per submatrix holding its column: at most ceil(K_w / s_w) times
+    const long long kc = (d->S + d->stride_w - 1) / d->stride_w;
+    if (ptr_cap) *ptr_cap = g.NC * (g.Ow + 1);
+    if (da_cap) *da_cap = g.NC * g.H * g.W * kc;
+    if (in_cap) *in_cap = g.NC * g.H * g.W * kc;
+    return SPC_OK;
+}
+
+spc_status cscc_encode(const spc_conv_desc* d, const float* x, spc_encoding* out, void* stream) {
+    spc_status s = check_cscc_geometry(d);
+    if (s != SPC_OK) return s;
+    if (!x || !out || !out->ptr || !out->da || !out->in || !out->chan_ptr_off || !out->chan_nz_off ||
+        !out->chan_in_off || !out->lengths)
+        return fail(SPC_EINVAL, "null pointer");
+    if (out->ptr_cap < 0 || out->da_cap < 0 || out->in_cap < 0) return fail(SPC_EINVAL, "negative capacity");
+    out->algo = SPC_ALGO_CSCC;
+    out->geom = *d;
+    return cuda_status(spc::launch_cscc_encode(spc::make_geom(*d), x, out, (cudaStream_t)stream), "cscc_encode");
+}
+
+spc_status cscc_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed, float* y,
+                             int32_t fuse_relu, void* stream) {
+    spc_status s = check_cscc_geometry(d);
+    if (s != SPC_OK) return s;
+    if (!enc || !w_packed || !y) return fail(SPC_EINVAL, "null pointer");
+    if (enc->algo != SPC_ALGO_CSCC) return fail(SPC_EINVAL, "not a CSCC encoding");
+    const spc_conv_desc& e = enc->geom;
+    if (e.N != d->N || e.C != d->C || e.H != d->H || e.W != d->W || e.R != d->R || e.S != d->S ||
+        e.stride_w != d->stride_w || e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom ||
+        e.pad_left != d->pad_left || e.pad_right != d->pad_right)
+        return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
+    return cuda_status(spc::launch_cscc_conv(spc::make_geom(*d), enc, w_packed, y, fuse_relu, (cudaStream_t)stream),
+                       "cscc_conv");
 }
 
 // ------------------------------------------------------------ selection
