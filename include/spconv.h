@@ -221,6 +221,26 @@ size_t spc_select_ws_bytes(const spc_conv_desc *d);
  * NaN times in the considered set or an unknown mode. */
 spc_status spc_select_from_times(const float *times_ms, int32_t sparse_ok, spc_mode mode, spc_algo *choice);
 
+/* ---- SI space bounds as a zero-cost pre-selector.
+ * All host-only, no GPU work.  Bounds are on the AVERAGE channel density rho_bar =
+ * sum_{n,c} rho_{n,c} / (I_n I_c) (reading A29; the printed bounds carry a factor I_n I_c and
+ * are then clipped to [0, 1]) in the SI's worst case (M = 1, VALID, no NPC, no NPF):
+ *   vs im2col / MEC (:616-640): the stride-agnostic CPO layout (reading
+ *     A15): O_w -> Ow1 = Wp - K_w + 1, ceil(K_w / s_w) -> K_w;
+ *   vs CSCC: (2 O_w K_w Hp rho_hat_bar + (O_w+1)(2 - ceil(K_w/s_w)) - 3)
+ *     / (2 H W), rho_hat_bar = the average per-image density of CSCC's lowered matrix (Eq. 17,
+ *     padded frame, readings A30 / A31). */
+typedef enum { SPC_SPACE_VS_IM2COL = 0, SPC_SPACE_VS_MEC = 1, SPC_SPACE_VS_CSCC = 2 } spc_space_vs;
+/* rho_bar_max = P(rho)'s upper end (rho_hat_bar is used only for SPC_SPACE_VS_CSCC). */
+spc_status spc_space_bound(const spc_conv_desc *d, spc_space_vs vs, double rho_hat_bar, double *rho_bar_max);
+/* Q(rho_hat): the least rho_hat_bar for which the CSCC bound is >= 0. */
+spc_status spc_cscc_q_bound(const spc_conv_desc *d, double *rho_hat_min);
+/* favour-space pre-selection without timing: SPC_ALGO_CPO when rho_bar <= the bound, else the
+ * dense comparison (SPC_ALGO_IM2COL, or SPC_ALGO_CSCC for vs = CSCC); geometries the sparse
+ * path rejects (pointwise, ...) always get the dense one. */
+spc_status spc_space_preselect(const spc_conv_desc *d, spc_space_vs vs, double rho_bar, double rho_hat_bar,
+                               spc_algo *choice);
+
 /* Host: output extents Oh = floor((H+pt+pb-R)/sh)+1, Ow = floor((W+pl+pr-S)/sw)+1
  * (reading A14) -- the dims every entry point uses for y. */
 spc_status spc_output_dims(const spc_conv_desc *d, int32_t *oh, int32_t *ow);

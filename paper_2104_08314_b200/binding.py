@@ -71,6 +71,9 @@ _sigs = {
     "spc_select_from_times": [ctypes.POINTER(ctypes.c_float), _i32, _i32, ctypes.POINTER(_i32)],
     "spc_output_dims": [_D, ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
     "spc_cscc_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "spc_space_bound": [_D, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
+    "spc_cscc_q_bound": [_D, ctypes.POINTER(ctypes.c_double)],
+    "spc_space_preselect": [_D, _i32, ctypes.c_double, ctypes.c_double, ctypes.POINTER(_i32)],
     "cscc_encode": [_D, _vp, _E, _vp],
     "cscc_conv_forward": [_D, _E, _vp, _vp, _i32, _vp],
 }
@@ -317,3 +320,26 @@ def cscc_conv_forward(d: dict, enc: Encoding, w_packed: torch.Tensor, y: torch.T
                       stream=None):
     _check(_lib.cscc_conv_forward(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(w_packed), _ptr(y),
                                   int(fuse_relu), _stream(stream)), "cscc_conv_forward")
+
+
+SPC_SPACE_VS_IM2COL, SPC_SPACE_VS_MEC, SPC_SPACE_VS_CSCC = 0, 1, 2
+
+
+def spc_space_bound(d: dict, vs: int, rho_hat_bar: float = 0.0) -> float:
+    out = ctypes.c_double()
+    _check(_lib.spc_space_bound(ctypes.byref(make_desc(d)), int(vs), float(rho_hat_bar), ctypes.byref(out)),
+           "spc_space_bound")
+    return out.value
+
+
+def spc_cscc_q_bound(d: dict) -> float:
+    out = ctypes.c_double()
+    _check(_lib.spc_cscc_q_bound(ctypes.byref(make_desc(d)), ctypes.byref(out)), "spc_cscc_q_bound")
+    return out.value
+
+
+def spc_space_preselect(d: dict, vs: int, rho_bar: float, rho_hat_bar: float = 0.0) -> int:
+    out = _i32()
+    _check(_lib.spc_space_preselect(ctypes.byref(make_desc(d)), int(vs), float(rho_bar), float(rho_hat_bar),
+                                    ctypes.byref(out)), "spc_space_preselect")
+    return out.value

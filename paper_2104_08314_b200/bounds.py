@@ -1,35 +1,26 @@
-"""Zero-cost space pre-selector from the SI's closed-form bounds (PAPER.md:590-640).
+"""Zero-cost space pre-selector from the SI's closed-form bounds (PAPER.md:590-689).
 
-P(rho): the average channel density below which the CPO encoding is no larger than the
-im2col lowered matrix (resp. the MEC lowered matrix), in the worst case the SI assumes
-(VALID padding, no NPC, no NPF).  Reading A29: the bound is on the average
-density rho_bar = sum_{n,c} rho_{n,c} / (I_n I_c).  Encoding geometry is stride-agnostic
-(reading A15): partitions O_w1 = W_p - K_w + 1 and ceil(K_w / s_w) -> K_w.
-
-Host-side arithmetic only (the oracle's copy lives in oracle/sizes.py; the two share no
-code and are compared in tests/test_bounds.py).
+Argument marshalling only: the arithmetic lives behind the C ABI (spc_space_bound,
+spc_cscc_q_bound, spc_space_preselect in include/spconv.h); the oracle's independent copy is
+oracle/sizes.py, and tests/test_bounds.py compares the two.
 """
 from __future__ import annotations
 
+from . import binding as B
 
-def _geom(d: dict):
-    wp = d["W"] + d["pad_left"] + d["pad_right"]
-    hp = d["H"] + d["pad_top"] + d["pad_bottom"]
-    return wp - d["S"] + 1, hp - d["R"] + 1
+_VS = {"im2col": B.SPC_SPACE_VS_IM2COL, "mec": B.SPC_SPACE_VS_MEC, "cscc": B.SPC_SPACE_VS_CSCC}
 
 
-def rho_space_bound(d: dict, vs: str = "im2col") -> float:
-    """Largest average density at which CPO is no larger than `vs` ("im2col" or "mec")."""
-    ow1, oh1 = _geom(d)
-    kw, kh, ih, iw = d["S"], d["R"], d["H"], d["W"]
-    inner = kw * kh * oh1 if vs == "im2col" else kw * ih
-    num = ow1 * (inner + 1 - kw) - 2 - kw
-    return min(1.0, max(0.0, num / (2.0 * ih * iw)))
+def rho_space_bound(d: dict, vs: str = "im2col", rho_hat_bar: float = 0.0) -> float:
+    """Largest average density at which CPO is no larger than `vs` ("im2col", "mec", "cscc")."""
+    return B.spc_space_bound(d, _VS[vs], rho_hat_bar)
 
 
-def space_preselect(d: dict, rho_bar: float, vs: str = "im2col") -> str:
-    """favour_space pre-selection without timing: 'cpo' when the measured average density
-    is inside P(rho), else the dense lowering."""
-    if d["R"] == 1 and d["S"] == 1:
-        return vs
-    return "cpo" if rho_bar <= rho_space_bound(d, vs) else vs
+def cscc_q_bound(d: dict) -> float:
+    """Q(rho_hat): least average lowered-matrix density with a non-empty CSCC bound."""
+    return B.spc_cscc_q_bound(d)
+
+
+def space_preselect(d: dict, rho_bar: float, vs: str = "im2col", rho_hat_bar: float = 0.0) -> str:
+    """favour-space pre-selection without timing: 'cpo' inside P(rho), else the dense method."""
+    return B.ALGO_NAMES[B.spc_space_preselect(d, _VS[vs], rho_bar, rho_hat_bar)]

@@ -324,6 +324,61 @@ spc_status cscc_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, co
                        "cscc_conv");
 }
 
+// ------------------------------------------------------------ SI space bounds (NEXT-3)
+
+namespace {
+double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+}
+
+spc_status spc_space_bound(const spc_conv_desc* d, spc_space_vs vs, double rho_hat_bar, double* rho_bar_max) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!rho_bar_max) return fail(SPC_EINVAL, "null pointer");
+    const spc::Geom g = spc::make_geom(*d);
+    const double HW = (double)d->H * d->W;
+    if (vs == SPC_SPACE_VS_IM2COL || vs == SPC_SPACE_VS_MEC) {
+        // PAPER.md:596-640 (reading A29): stride-agnostic encoding (A15), O_w -> Ow1, ceil -> K_w
+        const double inner = (vs == SPC_SPACE_VS_IM2COL) ? (double)d->S * d->R * g.Oh1 : (double)d->S * d->H;
+        *rho_bar_max = clip01((g.Ow1 * (inner + 1 - d->S) - 2 - d->S) / (2.0 * HW));
+        return SPC_OK;
+    }
+    if (vs == SPC_SPACE_VS_CSCC) {
+        // PAPER.md:663-684 (readings A30, A31): S_CSCC of Eq. 17 on the padded frame
+        if (!(rho_hat_bar >= 0.0 && rho_hat_bar <= 1.0)) return fail(SPC_EINVAL, "rho_hat_bar outside [0, 1]");
+        const int kc = (d->S + d->stride_w - 1) / d->stride_w;
+        *rho_bar_max = clip01((2.0 * g.Ow * d->S * g.Hp * rho_hat_bar + (double)(g.Ow + 1) * (2 - kc) - 3) / (2.0 * HW));
+        return SPC_OK;
+    }
+    return fail(SPC_EINVAL, "unknown comparison %d", (int)vs);
+}
+
+spc_status spc_cscc_q_bound(const spc_conv_desc* d, double* rho_hat_min) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (!rho_hat_min) return fail(SPC_EINVAL, "null pointer");
+    const spc::Geom g = spc::make_geom(*d);
+    const int kc = (d->S + d->stride_w - 1) / d->stride_w;
+    // Q(rho_hat), per image (reading A31)
+    *rho_hat_min = (3.0 - (double)(g.Ow + 1) * (2 - kc)) / (2.0 * g.Ow * g.Hp * d->S);
+    return SPC_OK;
+}
+
+spc_status spc_space_preselect(const spc_conv_desc* d, spc_space_vs vs, double rho_bar, double rho_hat_bar,
+                               spc_algo* choice) {
+    if (!choice) return fail(SPC_EINVAL, "null pointer");
+    double b = 0.0;
+    spc_status s = spc_space_bound(d, vs, rho_hat_bar, &b);
+    if (s != SPC_OK) return s;
+    const spc_algo dense = (vs == SPC_SPACE_VS_CSCC) ? SPC_ALGO_CSCC : SPC_ALGO_IM2COL;
+    if (check_sparse_geometry(d) != SPC_OK) {   // pointwise etc.: the sparse path does not apply
+        g_err.clear();
+        *choice = dense;
+        return SPC_OK;
+    }
+    *choice = (rho_bar <= b) ? SPC_ALGO_CPO : dense;
+    return SPC_OK;
+}
+
 // ------------------------------------------------------------ selection
 
 size_t spc_select_ws_bytes(const spc_conv_desc* d) {

@@ -5,7 +5,7 @@ import pytest
 
 import oracle
 from oracle import sizes
-from paper_2104_08314_b200.bounds import rho_space_bound, space_preselect
+from paper_2104_08314_b200.bounds import cscc_q_bound, rho_space_bound, space_preselect
 from synth import int_map, layer_desc
 
 SHAPES = [layer_desc(1, 3, 14, 14, 4, 3, 3, 1, 1, 0, 0, 0, 0), layer_desc(2, 2, 9, 11, 4, 3, 3, 1, 1, 0, 0, 0, 0),
@@ -66,6 +66,10 @@ def test_product_bound_equals_oracle(seed):
                    pl, pl)
     assert rho_space_bound(d, "im2col") == pytest.approx(sizes.p_bound_im2col(d), abs=1e-12)
     assert rho_space_bound(d, "mec") == pytest.approx(sizes.p_bound_mec(d), abs=1e-12)
+    d2 = dict(d, stride_w=int(rng.integers(1, 3)))
+    for rh in (0.0, 0.03, 0.2, 0.7):
+        assert rho_space_bound(d2, "cscc", rh) == pytest.approx(sizes.p_bound_cscc(d2, rh), abs=1e-12)
+    assert cscc_q_bound(d2) == pytest.approx(sizes.q_bound_cscc(d2), abs=1e-12)
 
 
 def test_preselector_routes_by_the_bound():
@@ -74,3 +78,6 @@ def test_preselector_routes_by_the_bound():
     assert space_preselect(d, rb * 0.9) == "cpo"
     assert space_preselect(d, min(1.0, rb * 1.1 + 1e-3)) in ("im2col", "cpo")
     assert space_preselect(layer_desc(1, 4, 8, 8, 4, 1, 1), 0.01) == "im2col"
+    q = cscc_q_bound(d)
+    assert space_preselect(d, 0.0, "cscc", max(0.0, q) + 0.05) == "cpo"
+    assert space_preselect(d, 1.0, "cscc", 0.0) == "cscc"
