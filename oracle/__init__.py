@@ -19,6 +19,8 @@ accumulation), which follows the paper step by step:
   cscc_encode        CSCC (SI Alg. 5 for any K_w, s_w)
   cscc_conv          CSCC conv (SI Alg. 6 + stride)
   cscc_decode        inverse of the CSCC streams            (test of the encoder)
+  encode_sa          stride-aware CPO layout (reading A32)  SI Eq. 2
+  decode_sa / sparse_conv_sa  its inverse and Alg. 2 over it
 
 Sizes (SI Eqs. 2-6, 11) are written out in ``sizes.py``.
 
@@ -89,6 +91,9 @@ def _L():
             "oc_cscc_encode": (ctypes.c_int, [P, vp, vp, i64, vp, i64, vp, i64, vp, vp]),
             "oc_cscc_conv": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp, vp]),
             "oc_cscc_decode": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp]),
+            "oc_encode_sa": (ctypes.c_int, [P, vp, vp, i64, vp, i64, vp, i64, vp, vp]),
+            "oc_decode_sa": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp]),
+            "oc_sparse_conv_sa": (ctypes.c_int, [P, vp, i64, vp, i64, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -282,3 +287,45 @@ def cscc_decode(d: dict, enc: Encoding) -> np.ndarray:
     if rc != 0:
         raise ValueError("corrupt CSCC streams")
     return x
+
+
+def encode_sa(d: dict, x: np.ndarray) -> Encoding:
+    """Stride-aware CPO layout (reading A32; SI Eq. 2's ceil(K_w/s_w) types)."""
+    x = _f32(x)
+    NC = d["N"] * d["C"]
+    _, Ow = out_hw(d)
+    cap_ptr = NC * (2 + d["S"] * (1 + Ow))
+    cap_da = max(1, x.size)
+    ptr = np.empty(cap_ptr, dtype=np.int32)
+    da = np.empty(cap_da, dtype=np.float32)
+    inn = np.empty(cap_da, dtype=np.int32)
+    off = np.empty(3 * (NC + 1), dtype=np.int64)
+    lens = np.zeros(3, dtype=np.int64)
+    rc = _L().oc_encode_sa(ctypes.byref(_desc(d)), _p(x), _p(ptr), cap_ptr, _p(da), cap_da, _p(inn), cap_da,
+                           _p(off), _p(lens))
+    if rc != 0:
+        raise RuntimeError(f"oracle encode_sa overflow, needed {lens.tolist()}")
+    off = off.reshape(3, NC + 1)
+    return Encoding(ptr=ptr[:lens[0]].copy(), da=da[:lens[1]].copy(), inn=inn[:lens[2]].copy(),
+                    chan_ptr_off=off[0].copy(), chan_nz_off=off[1].copy(), chan_in_off=off[2].copy(),
+                    cps=False, stride_aware=True)
+
+
+def decode_sa(d: dict, enc: Encoding) -> np.ndarray:
+    x = np.empty((d["N"], d["C"], d["H"], d["W"]), dtype=np.float32)
+    ptr, da = enc["ptr"], enc["da"]
+    if _L().oc_decode_sa(ctypes.byref(_desc(d)), _p(ptr), ptr.size, _p(da), da.size, _p(enc["inn"]), _p(x)) != 0:
+        raise ValueError("corrupt stride-aware streams")
+    return x
+
+
+def sparse_conv_sa(d: dict, enc: Encoding, w: np.ndarray) -> np.ndarray:
+    """Alg. 2 over the stride-aware layout: an NZE of partition s, type t feeds the t+1
+    partitions s..s+t covering its column (FP64)."""
+    Oh, Ow = out_hw(d)
+    y = np.empty((d["N"], d["K"], Oh, Ow), dtype=np.float64)
+    ptr, da = enc["ptr"], enc["da"]
+    if _L().oc_sparse_conv_sa(ctypes.byref(_desc(d)), _p(ptr), ptr.size, _p(da), da.size, _p(enc["inn"]),
+                              _p(_f32(w)), _p(y)) != 0:
+        raise ValueError("corrupt stride-aware streams")
+    return y

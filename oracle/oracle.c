@@ -709,3 +709,162 @@ int oc_cscc_decode(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const fl
         }
     return (p == n_ptr && z == n_da) ? 0 : -1;
 }
+
+/* ------------------------------------- stride-aware CPO layout (NEXT-4, reading A32) */
+
+/* SI Eq. 2 sizes the overlap pointer with ceil(K_w/s_w) types, i.e. a
+ * layout whose partitions are the O_w output columns at stride s_w -- which the paper never
+ * spells out (it encodes at stride 1).  Reading A32 makes it concrete for
+ * s_w >= 2: partition s (0 <= s < O_w) covers padded columns [s*s_w, s*s_w + K_w); column w
+ * has coverage cov(w) = #partitions covering it (0 .. ceil(K_w/s_w)); its owner is the first
+ * covering partition and its local column L = w - owner*s_w; its type is t = cov - 1.  Per
+ * channel: [NPC] if no covered column holds an NZE, else for every type t present in the
+ * geometry (ascending, as the paper orders NOP, overlap2, .. overlapK_w) the
+ * block [t+1, c_0 .. c_{O_w-1}] with block-relative cumulative counts through partition s's
+ * owned columns of type t (-1 if it owns none), or [t+1, NPF] if the block is empty.  DA / IN
+ * take the block's columns ascending, rows ascending, IN = L + h*K_w.  Columns no partition
+ * covers are never read by the convolution and are not stored. */
+static int32_t sa_ow(const oc_desc *d) { return oc_out_w(d); }
+
+static int32_t sa_cov(const oc_desc *d, int32_t w)
+{
+    int32_t n = 0;
+    for (int32_t s = 0; s < sa_ow(d); s++)
+        if (s * d->sw <= w && w < s * d->sw + d->S) n++;
+    return n;
+}
+
+static int32_t sa_owner(const oc_desc *d, int32_t w)
+{
+    for (int32_t s = 0; s < sa_ow(d); s++)
+        if (s * d->sw <= w && w < s * d->sw + d->S) return s;
+    return -1;
+}
+
+/* types present in the geometry: type t has at least one covered column */
+static int32_t sa_type_present(const oc_desc *d, int32_t t)
+{
+    int32_t Wp = d->W + d->pl + d->pr;
+    for (int32_t w = 0; w < Wp; w++)
+        if (sa_cov(d, w) == t + 1) return 1;
+    return 0;
+}
+
+static int32_t sa_ntypes(const oc_desc *d) { return (d->S + d->sw - 1) / d->sw; }
+
+int oc_encode_sa(const oc_desc *d, const float *x, int32_t *ptr, int64_t cap_ptr, float *da, int64_t cap_da,
+                 int32_t *in, int64_t cap_in, int64_t *chan_off, int64_t *lens)
+{
+    int32_t Hp = d->H + d->pt + d->pb, Wp = d->W + d->pl + d->pr, Ow = sa_ow(d), S = d->S;
+    int64_t np = 0, nz = 0, NC = (int64_t)d->N * d->C;
+    int overflow = 0;
+    int32_t *c = (int32_t *)malloc(sizeof(int32_t) * (size_t)Ow);
+#define PUSHP(v_) do { if (np < cap_ptr) ptr[np] = (v_); else overflow = 1; np++; } while (0)
+    for (int32_t n = 0; n < d->N; n++)
+        for (int32_t ch = 0; ch < d->C; ch++) {
+            int64_t j = (int64_t)n * d->C + ch;
+            if (chan_off) { chan_off[j] = np; chan_off[NC + 1 + j] = nz; chan_off[2 * (NC + 1) + j] = nz; }
+            const float *pl = plane_of(x, d, n, ch);
+            int32_t any = 0;
+            for (int32_t w = 0; w < Wp && !any; w++)
+                if (sa_cov(d, w) > 0)
+                    for (int32_t h = 0; h < Hp; h++) any |= I_at(pl, d, h, w) != 0.0f;
+            if (!any) { PUSHP(OC_NPC); continue; }
+            for (int32_t t = 0; t < sa_ntypes(d); t++) {
+                if (!sa_type_present(d, t)) continue;
+                int32_t nz_ptr = 0;
+                for (int32_t s = 0; s < Ow; s++) c[s] = -1;
+                for (int32_t w = 0; w < Wp; w++) {            /* the block's columns, ascending */
+                    if (sa_cov(d, w) != t + 1) continue;
+                    int32_t s = sa_owner(d, w), L = w - s * d->sw;
+                    for (int32_t h = 0; h < Hp; h++) {
+                        float v = I_at(pl, d, h, w);
+                        if (v != 0.0f) {
+                            if (nz < cap_da && nz < cap_in) { da[nz] = v; in[nz] = L + h * S; }
+                            else overflow = 1;
+                            nz++;
+                            nz_ptr++;
+                        }
+                    }
+                    c[s] = nz_ptr;                              /* cumulative through partition s */
+                }
+                PUSHP(t + 1);
+                if (nz_ptr == 0) PUSHP(OC_NPF);
+                else for (int32_t s = 0; s < Ow; s++) PUSHP(c[s]);
+            }
+        }
+#undef PUSHP
+    if (chan_off) { chan_off[NC] = np; chan_off[NC + 1 + NC] = nz; chan_off[2 * (NC + 1) + NC] = nz; }
+    lens[0] = np; lens[1] = nz; lens[2] = nz;
+    free(c);
+    return overflow ? -1 : 0;
+}
+
+/* Walk the stride-aware streams of one tensor and call back per NZE (n, c, s, t, index, v);
+ * mode 0 = decode into x, 1 = convolution into y.  Returns 0 or -1 (inconsistent). */
+static int sa_walk(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const float *da, int64_t n_da,
+                   const int32_t *in, float *x, const float *w, double *y)
+{
+    int32_t Hp = d->H + d->pt + d->pb, Ow = sa_ow(d), S = d->S, Oh = oc_out_h(d), Oh1 = Hp - d->R + 1;
+    int64_t p = 0, z = 0;
+    for (int32_t n = 0; n < d->N; n++)
+        for (int32_t ch = 0; ch < d->C; ch++) {
+            if (p >= n_ptr) return -1;
+            if (ptr[p] == OC_NPC) { p++; continue; }
+            for (int32_t t = 0; t < sa_ntypes(d); t++) {
+                if (!sa_type_present(d, t)) continue;
+                if (p + 1 >= n_ptr || ptr[p] != t + 1) return -1;
+                if (ptr[p + 1] == OC_NPF) { p += 2; continue; }
+                if (p + Ow >= n_ptr) return -1;
+                int32_t prev = 0;
+                for (int32_t s = 0; s < Ow; s++) {
+                    int32_t cs = ptr[p + 1 + s];
+                    if (cs < 0) continue;                     /* partition s owns no type-t column */
+                    if (cs < prev || z + cs > n_da) return -1;
+                    for (int32_t tx = prev; tx < cs; tx++) {
+                        int32_t e = in[z + tx], h = e / S, L = e % S, wcol = s * d->sw + L;
+                        double v = (double)da[z + tx];
+                        if (e < 0 || h >= Hp || sa_cov(d, wcol) != t + 1 || sa_owner(d, wcol) != s) return -1;
+                        if (x) {
+                            int32_t hh = h - d->pt, ww = wcol - d->pl;
+                            if (hh < 0 || hh >= d->H || ww < 0 || ww >= d->W) return -1;
+                            x[(((size_t)n * d->C + ch) * d->H + hh) * d->W + ww] = da[z + tx];
+                        } else {
+                            /* convSpMv over the t+1 partitions s..s+t that cover column wcol */
+                            for (int32_t k = 0; k < d->K; k++) {
+                                const float *wkc = w + ((size_t)k * d->C + ch) * d->R * d->S;
+                                double *O = y + ((size_t)n * d->K + k) * Oh * Ow;
+                                for (int32_t l = 0; l < d->R; l++) {
+                                    int32_t y1 = h - l;
+                                    if (y1 < 0 || y1 >= Oh1 || y1 % d->sh || y1 / d->sh >= Oh) continue;
+                                    for (int32_t i = 0; i <= t; i++) {
+                                        int32_t xo = s + i, m = wcol - xo * d->sw;
+                                        if (xo >= Ow || m < 0 || m >= S) continue;
+                                        O[(size_t)(y1 / d->sh) * Ow + xo] += v * (double)wkc[l * S + m];
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    prev = cs;
+                }
+                z += prev;
+                p += 1 + Ow;
+            }
+        }
+    return (p == n_ptr && z == n_da) ? 0 : -1;
+}
+
+int oc_decode_sa(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const float *da, int64_t n_da,
+                 const int32_t *in, float *x)
+{
+    memset(x, 0, sizeof(float) * (size_t)d->N * d->C * d->H * d->W);
+    return sa_walk(d, ptr, n_ptr, da, n_da, in, x, NULL, NULL);
+}
+
+int oc_sparse_conv_sa(const oc_desc *d, const int32_t *ptr, int64_t n_ptr, const float *da, int64_t n_da,
+                      const int32_t *in, const float *w, double *y)
+{
+    memset(y, 0, sizeof(double) * (size_t)d->N * d->K * oc_out_h(d) * oc_out_w(d));
+    return sa_walk(d, ptr, n_ptr, da, n_da, in, NULL, w, y);
+}

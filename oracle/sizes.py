@@ -171,3 +171,30 @@ def s_cpo_worst_kc(d: dict, rho_bar: float) -> float:
     I_n I_c (3 + (kc - 1)(1 + O_w)) + 2 H W I_n I_c rho_bar."""
     ow, kc = _ow(d), _kc(d)
     return d["N"] * d["C"] * (3 + (kc - 1) * (1 + ow)) + 2.0 * d["H"] * d["W"] * d["N"] * d["C"] * rho_bar
+
+
+# ---- stride-aware layout (reading A32, NEXT-4) ----------------------------------------
+
+def sa_column_cover(d: dict) -> np.ndarray:
+    """cov(w) of every padded column: output partitions s (stride s_w) with s*s_w <= w < s*s_w + K_w."""
+    Wp = d["W"] + d["pad_left"] + d["pad_right"]
+    cov = np.zeros(Wp, np.int64)
+    for s in range(_ow(d)):
+        cov[s * d["stride_w"]: s * d["stride_w"] + d["S"]] += 1
+    return cov
+
+
+def ptr_size_sa(d: dict, live_channels: int, count_npf: int) -> int:
+    """ptr length of the stride-aware layout in the form of SI Eq. 3:
+    every live channel carries one (1 + O_w) block per coverage type present -- the
+    coverage-1 block (the NOP generalisation) plus Eq. 2's ceil(K_w/s_w) - 1 overlap blocks
+    (M = 1) -- each NPF block saving O_w - 1 entries; a dead channel is one NPC entry."""
+    ow = _ow(d)
+    types = len(set(int(c) for c in sa_column_cover(d)) - {0})
+    nc = d["N"] * d["C"]
+    return (nc - live_channels) + live_channels * types * (1 + ow) - count_npf * (ow - 1)
+
+
+def op_size_eq2_strided(d: dict) -> int:
+    """SI Eq. 2 as printed with M = 1: (ceil(K_w/s_w) - 1)(1 + O_w), O_w at the real stride."""
+    return (_kc(d) - 1) * (1 + _ow(d))
