@@ -48,7 +48,8 @@ typedef enum {
 } spc_status;
 
 typedef enum { SPC_ALGO_IM2COL = 0, SPC_ALGO_CPO = 1, SPC_ALGO_CPS = 2,
-               SPC_ALGO_CSCC = 3 /* the paper's comparison baseline (cscc_encode), never selected */ } spc_algo;
+               SPC_ALGO_CSCC = 3,   /* the paper's comparison baseline (cscc_encode), never selected */
+               SPC_ALGO_CPO_SA = 4  /* stride-aware CPO layout (cpo_encode_strided, reading A32) */ } spc_algo;
 
 /* Hybrid selection modes: favour time = argmin{im2col, CPO};
  * favour space = argmin{im2col, CPS}; best of three = argmin over all three. */
@@ -144,6 +145,23 @@ spc_status spc_pack_weights(const spc_conv_desc *d, const float *w_kcrs, float *
  * launch reduces its partial sums through L2 instead of distributed shared memory). */
 spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
                                float *y, int32_t fuse_relu, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- Stride-aware CPO layout (reading A32 of DESIGN.md).  SI Eq. 2
+ * sizes the overlap pointer with ceil(K_w/s_w) types, i.e. partitions at the
+ * real horizontal stride; the paper encodes at stride 1 only.  Here partition s
+ * (0 <= s < O_w) covers padded columns [s*s_w, s*s_w + K_w); a column's type t = (number of
+ * partitions covering it) - 1, owner = the first of them, local column L = w - owner*s_w.  Per
+ * channel: [NPC] if no covered column holds an NZE, else for each type present (ascending)
+ * [t+1, c_0 .. c_{O_w-1}] (block-relative cumulative counts through partition s's owned type-t
+ * columns, -1 = owns none) or [t+1, NPF]; DA / IN column by column ascending, rows ascending,
+ * IN = L + h*K_w.  Columns no partition covers are not stored (no output reads them).  At
+ * s_w = 2 a block holds O_w instead of Wp - K_w + 1 partitions (about half the ptr).
+ * algo = SPC_ALGO_CPO_SA; sparse_conv_forward accepts it (the encoding's stride_w must equal
+ * the descriptor's).  Capacities: ptr <= N*C*max(1, ceil(K_w/s_w)*(1+O_w)), da = in <= N*C*H*W. */
+spc_status spc_strided_capacity(const spc_conv_desc *d, int64_t *ptr_cap, int64_t *da_cap, int64_t *in_cap);
+/* Three launches (counts, scan, writes); lengths[3] = 1 (nothing written) when a capacity is
+ * too small.  SPC_EUNSUPPORTED: pointwise, K_w > 8, or a plane too large for one CTA. */
+spc_status cpo_encode_strided(const spc_conv_desc *d, const float *x, spc_encoding *out, void *stream);
 
 /* ---- CSCC, the paper's comparison method.
  * Encoding = SI Alg. 5, the paper's simplification of the CSCC encoder

@@ -23,11 +23,11 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 SPC_OK, SPC_EINVAL, SPC_EUNSUPPORTED, SPC_ECAPACITY, SPC_ECUDA, SPC_ECORRUPT = 0, -1, -2, -3, -4, -5
-SPC_ALGO_IM2COL, SPC_ALGO_CPO, SPC_ALGO_CPS, SPC_ALGO_CSCC = 0, 1, 2, 3
+SPC_ALGO_IM2COL, SPC_ALGO_CPO, SPC_ALGO_CPS, SPC_ALGO_CSCC, SPC_ALGO_CPO_SA = 0, 1, 2, 3, 4
 SPC_FAVOUR_TIME, SPC_FAVOUR_SPACE, SPC_BEST_OF_THREE = 0, 1, 2
 SPC_NPC = -(2 ** 31)
 SPC_NPF = -(2 ** 31) + 1
-ALGO_NAMES = {0: "im2col", 1: "cpo", 2: "cps", 3: "cscc"}
+ALGO_NAMES = {0: "im2col", 1: "cpo", 2: "cps", 3: "cscc", 4: "cpo_sa"}
 
 
 class SpcError(RuntimeError):
@@ -72,6 +72,8 @@ _sigs = {
     "spc_output_dims": [_D, ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
     "spc_cscc_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "spc_space_bound": [_D, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
+    "spc_strided_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "cpo_encode_strided": [_D, _vp, _E, _vp],
     "spc_cscc_q_bound": [_D, ctypes.POINTER(ctypes.c_double)],
     "spc_space_preselect": [_D, _i32, ctypes.c_double, ctypes.c_double, ctypes.POINTER(_i32)],
     "cscc_encode": [_D, _vp, _E, _vp],
@@ -343,3 +345,19 @@ def spc_space_preselect(d: dict, vs: int, rho_bar: float, rho_hat_bar: float = 0
     _check(_lib.spc_space_preselect(ctypes.byref(make_desc(d)), int(vs), float(rho_bar), float(rho_hat_bar),
                                     ctypes.byref(out)), "spc_space_preselect")
     return out.value
+
+
+def spc_strided_capacity(d: dict) -> tuple[int, int, int]:
+    p, a, i = _i64(), _i64(), _i64()
+    _check(_lib.spc_strided_capacity(ctypes.byref(make_desc(d)), ctypes.byref(p), ctypes.byref(a), ctypes.byref(i)),
+           "spc_strided_capacity")
+    return p.value, a.value, i.value
+
+
+def alloc_strided_encoding(d: dict, device="cuda") -> Encoding:
+    return alloc_cscc_encoding(d, device, caps=spc_strided_capacity(d))
+
+
+def cpo_encode_strided(d: dict, x: torch.Tensor, enc: Encoding, stream=None):
+    _check(_lib.cpo_encode_strided(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _stream(stream)),
+           "cpo_encode_strided")

@@ -1,5 +1,6 @@
 // api.cu -- extern "C" entry points of libspconv.so (declared in include/spconv.h).
 // Host-side validation, workspace carving, launches and the offline selector.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +15,11 @@ size_t cscc_smem_bytes(const Geom& g);
 cudaError_t launch_cscc_encode(const Geom& g, const float* x, spc_encoding* e, cudaStream_t st);
 cudaError_t launch_cscc_conv(const Geom& g, const spc_encoding* e, const float* w_packed, float* y, int relu,
                              cudaStream_t st);
+size_t sa_smem_bytes(const Geom& g);
+int sa_types(const Geom& g);
+cudaError_t launch_sa_encode(const Geom& g, const float* x, spc_encoding* e, cudaStream_t st);
+cudaError_t launch_sa_conv(const Geom& g, const spc_encoding* e, const float* w_packed, float* y, int relu,
+                           cudaStream_t st);
 cudaError_t launch_validate(const Geom& g, const spc_encoding* e, void* rec_dev, cudaStream_t st,
                             long long* bad_channel, int* code);
 }
@@ -158,7 +164,8 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
     spc_status s = check_sparse_geometry(d);
     if (s != SPC_OK) return s;
     if (!enc || !w_packed || !y) return fail(SPC_EINVAL, "null pointer");
-    if (enc->algo != SPC_ALGO_CPO && enc->algo != SPC_ALGO_CPS) return fail(SPC_EINVAL, "not a CPO / CPS encoding");
+    if (enc->algo != SPC_ALGO_CPO && enc->algo != SPC_ALGO_CPS && enc->algo != SPC_ALGO_CPO_SA)
+        return fail(SPC_EINVAL, "not a CPO / CPS / stride-aware CPO encoding");
     const spc_conv_desc& e = enc->geom;
     if (e.N != d->N || e.C != d->C || e.H != d->H || e.W != d->W || e.R != d->R || e.S != d->S ||
         e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom || e.pad_left != d->pad_left ||
@@ -166,6 +173,12 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
         return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
     spc::Geom g = spc::make_geom(*d);
     cudaStream_t st = (cudaStream_t)stream;
+    if (enc->algo == SPC_ALGO_CPO_SA) {
+        // the layout depends on the horizontal stride (reading A32)
+        if (e.stride_w != d->stride_w) return fail(SPC_EINVAL, "stride-aware encoding made for another stride");
+        if ((size_t)4 * g.Oh * 32 * 8 > 227 * 1024) return fail(SPC_EUNSUPPORTED, "output too tall");
+        return cuda_status(spc::launch_sa_conv(g, enc, w_packed, y, fuse_relu, st), "sparse_conv (stride-aware)");
+    }
     const int32_t* in_cpo = nullptr;
     if (enc->algo == SPC_ALGO_CPS && d->S > 1) {
         spc::WsLayout L = spc::ws_layout(g);
@@ -322,6 +335,34 @@ spc_status cscc_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, co
         return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
     return cuda_status(spc::launch_cscc_conv(spc::make_geom(*d), enc, w_packed, y, fuse_relu, (cudaStream_t)stream),
                        "cscc_conv");
+}
+
+// ------------------------------------------------------------ stride-aware CPO layout (NEXT-4)
+
+spc_status spc_strided_capacity(const spc_conv_desc* d, int64_t* ptr_cap, int64_t* da_cap, int64_t* in_cap) {
+    spc_status s = check_desc(d);
+    if (s != SPC_OK) return s;
+    if (d->R == 1 && d->S == 1) return fail(SPC_EUNSUPPORTED, "pointwise kernels are routed to im2col (PAPER.md:123)");
+    if (d->S > 8) return fail(SPC_EUNSUPPORTED, "K_w > 8 not supported");
+    const spc::Geom g = spc::make_geom(*d);
+    if (spc::sa_smem_bytes(g) > 227 * 1024) return fail(SPC_EUNSUPPORTED, "plane too large for one CTA");
+    if ((long long)(d->S - 1) + (long long)(g.Hp - 1) * d->S >= (1ll << 31)) return fail(SPC_EUNSUPPORTED, "index overflow");
+    if (ptr_cap) *ptr_cap = g.NC * std::max<long long>(1, (long long)spc::sa_types(g) * (1 + g.Ow));
+    if (da_cap) *da_cap = g.NC * g.H * g.W;
+    if (in_cap) *in_cap = g.NC * g.H * g.W;
+    return SPC_OK;
+}
+
+spc_status cpo_encode_strided(const spc_conv_desc* d, const float* x, spc_encoding* out, void* stream) {
+    spc_status s = spc_strided_capacity(d, nullptr, nullptr, nullptr);
+    if (s != SPC_OK) return s;
+    if (!x || !out || !out->ptr || !out->da || !out->in || !out->chan_ptr_off || !out->chan_nz_off ||
+        !out->chan_in_off || !out->lengths)
+        return fail(SPC_EINVAL, "null pointer");
+    if (out->ptr_cap < 0 || out->da_cap < 0 || out->in_cap < 0) return fail(SPC_EINVAL, "negative capacity");
+    out->algo = SPC_ALGO_CPO_SA;
+    out->geom = *d;
+    return cuda_status(spc::launch_sa_encode(spc::make_geom(*d), x, out, (cudaStream_t)stream), "cpo_encode_strided");
 }
 
 // ------------------------------------------------------------ SI space bounds (NEXT-3)
