@@ -183,6 +183,20 @@ spc_status cscc_encode(const spc_conv_desc *d, const float *x, spc_encoding *out
 spc_status cscc_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed, float *y,
                              int32_t fuse_relu, void *stream);
 
+/* NEXT-1: the convolution emits its output ALREADY CPO-encoded
+ * for the next layer.  Computes y exactly as sparse_conv_forward (ReLU if fuse_relu; y is still
+ * written) and, in the same kernel's epilogue, a row bitmask per output column of the non-zero
+ * outputs; three small launches then build the CPO streams of y for the layer `next` (whose
+ * input is y: next->N == N, next->C == K, next->H == Oh, next->W == Ow) from the masks, reading
+ * only y's NZEs -- bit-identical to cpo_encode(next, y) (no dense re-scan of y).  `out` as for
+ * cpo_encode (algo = SPC_ALGO_CPO).  ws: >= spc_fused_ws_bytes(d), zeroed once
+ * (spc_workspace_init), one stream at a time.  SPC_EUNSUPPORTED: next's padded height > 64 or
+ * padded width > 256, or a stride-aware input encoding. */
+size_t spc_fused_ws_bytes(const spc_conv_desc *d);
+spc_status sparse_conv_encode_forward(const spc_conv_desc *d, const spc_encoding *enc, const float *w_packed,
+                                      float *y, int32_t fuse_relu, const spc_conv_desc *next, spc_encoding *out,
+                                      void *ws, size_t ws_bytes, void *stream);
+
 /* Dense baseline: im2col lowering of x into ws_lowered (SI Eq. 6
  * elements, fp32), then y[n] = W[K x CRS] * L[n].  Layout: [N][C*R*S][Oh*Ow] for the
  * cuBLAS / SIMT engines, [N*Oh*Ow][C*R*S] (K-major, one GEMM over all images) for the

@@ -74,6 +74,7 @@ _sigs = {
     "spc_space_bound": [_D, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
     "spc_strided_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "cpo_encode_strided": [_D, _vp, _E, _vp],
+    "sparse_conv_encode_forward": [_D, _E, _vp, _vp, _i32, _D, _E, _vp, _sz, _vp],
     "spc_cscc_q_bound": [_D, ctypes.POINTER(ctypes.c_double)],
     "spc_space_preselect": [_D, _i32, ctypes.c_double, ctypes.c_double, ctypes.POINTER(_i32)],
     "cscc_encode": [_D, _vp, _E, _vp],
@@ -90,12 +91,14 @@ _lib.spc_im2col_engine.argtypes = [ctypes.c_void_p]
 _lib.spc_im2col_engine.restype = ctypes.c_int
 _lib.spc_im2col_ws_bytes.argtypes = [ctypes.c_void_p]
 _lib.spc_im2col_ws_bytes.restype = ctypes.c_size_t
+_lib.spc_fused_ws_bytes.argtypes = [_D]
+_lib.spc_fused_ws_bytes.restype = _sz
 _lib.spc_select_ws_bytes.argtypes = [_D]
 _lib.spc_select_ws_bytes.restype = _sz
 _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
-EXPORTED = list(_sigs) + ["spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
+EXPORTED = list(_sigs) + ["spc_fused_ws_bytes", "spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
                           "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes"]
 SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
 SPC_GEMM_AUTO = 5
@@ -361,3 +364,17 @@ def alloc_strided_encoding(d: dict, device="cuda") -> Encoding:
 def cpo_encode_strided(d: dict, x: torch.Tensor, enc: Encoding, stream=None):
     _check(_lib.cpo_encode_strided(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _stream(stream)),
            "cpo_encode_strided")
+
+
+def alloc_fused_workspace(d: dict, device="cuda") -> torch.Tensor:
+    """Workspace of sparse_conv_encode_forward (conv workspace + output masks), zeroed once."""
+    ws = torch.empty(int(_lib.spc_fused_ws_bytes(ctypes.byref(make_desc(d)))), dtype=torch.uint8, device=device)
+    spc_workspace_init(ws)
+    return ws
+
+
+def sparse_conv_encode_forward(d: dict, enc: Encoding, w_packed: torch.Tensor, y: torch.Tensor, fuse_relu: bool,
+                               next_d: dict, out: Encoding, ws: torch.Tensor, stream=None):
+    _check(_lib.sparse_conv_encode_forward(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(w_packed), _ptr(y),
+                                           int(fuse_relu), ctypes.byref(make_desc(next_d)), ctypes.byref(out.c),
+                                           _ptr(ws), ws.numel(), _stream(stream)), "sparse_conv_encode_forward")

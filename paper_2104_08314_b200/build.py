@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspconv.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "encode.cu", "sparse_conv.cu", "im2col.cu", "tcgemm.cu", "validate.cu", "cscc.cu", "stride_aware.cu"]
+SOURCES = ["api.cu", "encode.cu", "sparse_conv.cu", "im2col.cu", "tcgemm.cu", "validate.cu", "cscc.cu", "stride_aware.cu", "fused_encode.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

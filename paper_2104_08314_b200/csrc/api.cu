@@ -18,6 +18,8 @@ cudaError_t launch_cscc_conv(const Geom& g, const spc_encoding* e, const float* 
 size_t sa_smem_bytes(const Geom& g);
 int sa_types(const Geom& g);
 cudaError_t launch_sa_encode(const Geom& g, const float* x, spc_encoding* e, cudaStream_t st);
+cudaError_t launch_encode_from_masks(const Geom& gn, const float* y, unsigned long long* omask, spc_encoding* e,
+                                     cudaStream_t st);
 cudaError_t launch_sa_conv(const Geom& g, const spc_encoding* e, const float* w_packed, float* y, int relu,
                            cudaStream_t st);
 cudaError_t launch_validate(const Geom& g, const spc_encoding* e, void* rec_dev, cudaStream_t st,
@@ -159,8 +161,11 @@ spc_status spc_pack_weights(const spc_conv_desc* d, const float* w_kcrs, float* 
     return cuda_status(spc::launch_pack_weights(g, w_kcrs, w_packed, (cudaStream_t)stream), "pack_weights");
 }
 
-spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed, float* y,
-                               int32_t fuse_relu, void* ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+spc_status conv_impl(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed, float* y,
+                     int32_t fuse_relu, void* ws, size_t ws_bytes, void* stream, unsigned long long* omask) {
     spc_status s = check_sparse_geometry(d);
     if (s != SPC_OK) return s;
     if (!enc || !w_packed || !y) return fail(SPC_EINVAL, "null pointer");
@@ -177,6 +182,7 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
         // the layout depends on the horizontal stride (reading A32)
         if (e.stride_w != d->stride_w) return fail(SPC_EINVAL, "stride-aware encoding made for another stride");
         if ((size_t)4 * g.Oh * 32 * 8 > 227 * 1024) return fail(SPC_EUNSUPPORTED, "output too tall");
+        if (omask) return fail(SPC_EUNSUPPORTED, "fused encode: CPO / CPS input encodings only");
         return cuda_status(spc::launch_sa_conv(g, enc, w_packed, y, fuse_relu, st), "sparse_conv (stride-aware)");
     }
     const int32_t* in_cpo = nullptr;
@@ -197,8 +203,47 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
             scratch_bytes = L.total - L.scratch;
         }
     }
-    return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, scratch, scratch_bytes, st),
+    return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, scratch, scratch_bytes, st, omask),
                        "sparse_conv");
+}
+}  // namespace
+
+extern "C" {
+
+spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed, float* y,
+                               int32_t fuse_relu, void* ws, size_t ws_bytes, void* stream) {
+    return conv_impl(d, enc, w_packed, y, fuse_relu, ws, ws_bytes, stream, nullptr);
+}
+
+size_t spc_fused_ws_bytes(const spc_conv_desc* d) {
+    if (check_sparse_geometry(d) != SPC_OK) return 0;
+    const spc::Geom g = spc::make_geom(*d);
+    return spc::align_up(spc::ws_layout(g).total, 256) + spc::align_up((size_t)8 * g.N * g.K * g.Ow, 256);
+}
+
+spc_status sparse_conv_encode_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed,
+                                      float* y, int32_t fuse_relu, const spc_conv_desc* next, spc_encoding* out,
+                                      void* ws, size_t ws_bytes, void* stream) {
+    spc_status s = check_sparse_geometry(next);
+    if (s != SPC_OK) return s;
+    s = check_sparse_geometry(d);
+    if (s != SPC_OK) return s;
+    const spc::Geom g = spc::make_geom(*d), gn = spc::make_geom(*next);
+    if (next->N != d->N || next->C != d->K || next->H != g.Oh || next->W != g.Ow)
+        return fail(SPC_EINVAL, "next layer's input must be this layer's output (N, K, Oh, Ow)");
+    if (gn.Hp > 64 || gn.Wp > 256) return fail(SPC_EUNSUPPORTED, "fused encode: padded height <= 64, width <= 256");
+    if (!out || !out->ptr || !out->da || !out->in || !out->chan_ptr_off || !out->chan_nz_off || !out->chan_in_off ||
+        !out->lengths || !ws)
+        return fail(SPC_EINVAL, "null pointer");
+    const size_t need = spc_fused_ws_bytes(d);
+    if (ws_bytes < need) return fail(SPC_EINVAL, "fused workspace too small (%zu < %zu)", ws_bytes, need);
+    const size_t mo = spc::align_up(spc::ws_layout(g).total, 256);
+    unsigned long long* omask = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + mo);
+    s = conv_impl(d, enc, w_packed, y, fuse_relu, ws, mo, stream, omask);
+    if (s != SPC_OK) return s;
+    out->algo = SPC_ALGO_CPO;
+    out->geom = *next;
+    return cuda_status(spc::launch_encode_from_masks(gn, y, omask, out, (cudaStream_t)stream), "encode_from_masks");
 }
 
 spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const float* w_kcrs, float* y,

@@ -387,6 +387,8 @@ struct ConvArgs {
     unsigned* sk_flags;   // balanced mode: one "partial published" flag per CTA (zeroed after use)
     unsigned long long* status;   // the encoding's overflow word (lengths[3]): nonzero -> y = 0;
                                   // a balanced-mode wait timeout sets bit 2
+    unsigned long long* omask;    // NEXT-1 fused encode: per output column (n, k, x) a bit per output
+                                  // row holding an NZE of y (null = off); zeroed by its consumer
     int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
     int sk_strips;        // balanced mode: column strips per image (unit = (k-block, image, strip))
     long long sk_units;   // balanced mode: strips x images x k-blocks
@@ -439,6 +441,18 @@ __device__ __forceinline__ float4 lds128(const float4* p) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"((unsigned)__cvta_generic_to_shared(p)));
     return v;
 }
+// NEXT-1 (fused encode): mark the non-zero outputs of a 4-column output row chunk in the
+// per-column row masks of y (consumed by encode_from_masks, which re-zeroes them)
+__device__ __forceinline__ void emit_omask(unsigned long long* omask, const Geom& g, int n, int k, int oy, int ox0,
+                                           const float4& v) {
+    if (!omask) return;
+    const float sv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+        if (ox0 + q < g.Ow && sv[q] != 0.0f)
+            atomicOr(omask + ((long long)n * g.K + k) * g.Ow + ox0 + q, 1ull << oy);
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
@@ -969,6 +983,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     if (k >= g.K || oy >= g.Oh) continue;
                     float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
                     if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+                    emit_omask(a.omask, g, n, k, oy, ox0, v);
                     float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
                     if (vec_ok && ox0 + 3 < g.Ow) {
                         if (add)
@@ -1091,6 +1106,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 const int c = ci / rows, row = ci % rows, kl = row & (T::KB - 1);   // kl = j*32 + lane
                 const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = (row / T::KB) * T::TY + c;
                 if (k >= g.K || oy >= g.Oh) continue;
+                emit_omask(a.omask, g, n, k, oy, ox0, sum);
                 float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
                 if (vec_ok && ox0 + 3 < g.Ow) {
                     *reinterpret_cast<float4*>(dst) = sum;
@@ -1138,6 +1154,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             const int kl = row & (T::KB - 1), rr = row / T::KB;   // kl = j*32 + lane
             const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = rr * T::TY + c;   // chunk c = output row c
             if (k >= g.K || oy >= g.Oh) continue;
+            emit_omask(a.omask, g, n, k, oy, ox0, sum);
             float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
             if (vec_ok && ox0 + 3 < g.Ow) {
                 *reinterpret_cast<float4*>(dst) = sum;
@@ -1209,6 +1226,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
         float s = 0.f;
         for (int wv = 0; wv < kGenWarps; wv++) s += accs[(wv * kGenTY * kGenTX + yy * kGenTX + xx) * 32 + kl];
         if (a.relu) s = fmaxf(s, 0.f);
+        if (a.omask && s != 0.0f) atomicOr(a.omask + ((long long)n * g.K + kk) * g.Ow + ox, 1ull << oy);
         a.y[(((long long)n * g.K + kk) * g.Oh + oy) * g.Ow + ox] = s;
     }
 }
@@ -1410,7 +1428,7 @@ size_t conv_scratch_bytes(const Geom& g) {
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
-                               cudaStream_t st) {
+                               cudaStream_t st, unsigned long long* omask) {
     ConvArgs a;
     a.g = g;
     a.ptr = e->ptr;
@@ -1422,6 +1440,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.y = y;
     a.relu = relu;
     a.status = reinterpret_cast<unsigned long long*>(e->lengths + 3);
+    a.omask = omask;
     a.tiles_x = 1;
     a.cg = 1;
     a.rt = 1;

@@ -422,8 +422,9 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
     const bool vec_ok = (g.Ow % 4) == 0;
     const int cw = warp - T::NPROD;
     const int rtile = producer ? 0 : cw % RT, kg = producer ? 0 : cw / RT;
-    auto store4 = [&](float* dst, float4 v) {
+    auto store4 = [&](float* dst, float4 v, int k, int oy) {
         if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+        emit_omask(a.omask, g, n, k, oy, ox0, v);
         if (vec_ok && ox0 + 3 < g.Ow) {
             *reinterpret_cast<float4*>(dst) = v;
         } else {
@@ -451,7 +452,7 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
             for (int i = 0; i < T::NACC / 4; i++) {
                 const int k = kbase + kg * T::KB + lane * T::KPL + (i / NCH), oy = rtile * T::TY + (i % NCH);
                 if (k >= g.K || oy >= g.Oh) continue;
-                store4(yb + ((long long)k * g.Oh + oy) * g.Ow + ox0, accv(i));
+                store4(yb + ((long long)k * g.Oh + oy) * g.Ow + ox0, accv(i), k, oy);
             }
         }
         return;
@@ -487,7 +488,7 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
         const int kgi = kl / T::KB, kin = kl % T::KB;
         const int k = kbase + kgi * T::KB + (kin & 31) * T::KPL + (kin >> 5), oy = rt * T::TY + c;
         if (k >= g.K || oy >= g.Oh) continue;
-        store4(yb + ((long long)k * g.Oh + oy) * g.Ow + ox0, sum);
+        store4(yb + ((long long)k * g.Oh + oy) * g.Ow + ox0, sum, k, oy);
     }
 }
 
