@@ -306,8 +306,8 @@ class Rotating:
                     L.conv()
                 elif kind == "cps":
                     L.forward(x, "cps")
-                elif kind == "im2col":
-                    L.forward(x, "im2col")
+                elif kind in ("im2col", "cscc", "cpo_sa"):
+                    L.forward(x, kind)
         # warm the buffers (lowered workspaces, the encodings the conv-only graph reads)
         body()
         torch.cuda.synchronize()
@@ -407,6 +407,97 @@ def measure_layer(name, d, pool, w, dev, stream, steps, hbm_gbs, p_fp32, im2col=
     return row, R
 
 
+def measure_extra(name, d, pool, w, dev, stream, steps, kinds):
+    """Other encodings of the same layer, back to back over rotating sets: the CSCC baseline
+    (the paper's comparison method) and the stride-aware layout; step us and CR vs S_im2col."""
+    R = Rotating(d, pool, w, dev)
+    Oh, Ow = spc_out_hw(d)
+    s_im2col = d["N"] * Oh * Ow * d["C"] * d["R"] * d["S"]
+    row = {"workload": name}
+    for k in kinds:
+        row[f"{k}_step_us"] = R.timed(k, steps, stream) / steps * 1e3
+        L0 = R.layers[0]
+        L0.forward(R.xs[0], k)
+        import paper_2104_08314_b200 as spc
+        p, a, i = spc.spc_encoding_lengths(L0.extra_encoding(k))
+        row[f"cr_{k}"] = s_im2col / (p + a + i)
+        row[f"{k}_ptr"] = p
+    row["cpo_step_us"] = R.timed("step", steps, stream) / steps * 1e3
+    L0 = R.layers[0]
+    L0.forward(R.xs[0], "cpo")
+    p, a, i = L0.lengths()
+    row["cr_cpo"] = s_im2col / (p + a + i)
+    row["cpo_ptr"] = p
+    row["l2"] = R.l2_note()
+    return row
+
+
+def measure_fused_chain(dev, stream, steps, rank=0):
+    """NEXT-1 on the cfg4 chain (1x7 -> ReLU -> 7x1, BASELINE.json configs[3]): layer 1's conv
+    emitting layer 2's CPO encoding (sparse_conv_encode_forward) against conv + a separate
+    cpo_encode of the dense intermediate; both followed by layer 2's conv.  Back to back over
+    rotating buffer sets (each set > L2 / NSET)."""
+    import torch
+
+    import paper_2104_08314_b200 as spc
+    from paper_2104_08314_b200.layer import SparseConvLayer
+    a, b = CONFIGS["cfg4a"], CONFIGS["cfg4b"]
+    d1, d2 = a["desc"], b["desc"]
+    pool = make_pool(a, rank)
+    w1 = he_normal(d1["K"], d1["C"], 1, 7, a["seed"])
+    w2 = he_normal(d2["K"], d2["C"], 7, 1, b["seed"] + 1)
+    touched = 4 * (2 * pool[0].size * d1["N"] + w1.size + w2.size) + 8 * 0.5 * pool[0].size * d1["N"]
+    nset = int(min(64, max(4, np.ceil(1.5 * L2_BYTES / touched))))
+    sets = []
+    for i in range(nset):
+        idx = [(i + j) % pool.shape[0] for j in range(d1["N"])]
+        x = torch.from_numpy(np.ascontiguousarray(pool[idx])).to(dev)
+        L1 = SparseConvLayer(d1, torch.from_numpy(w1).to(dev), device=dev, relu=True)
+        L2 = SparseConvLayer(d2, torch.from_numpy(w2).to(dev), device=dev)
+        out = spc.alloc_encoding(d2, device=dev)
+        fws = spc.alloc_fused_workspace(d1, device=dev)
+        L1.encode(x)
+        sets.append((x, L1, L2, out, fws))
+
+    def run(kind, n):
+        for i in range(n):
+            x, L1, L2, out, fws = sets[i % nset]
+            if kind == "separate":      # conv 1 (ReLU) -> encode y1 -> conv 2
+                L1.conv()
+                L2.encode(L1.y)
+                L2.conv()
+            elif kind == "fused":       # conv 1 emitting layer 2's encoding -> conv 2
+                spc.sparse_conv_encode_forward(d1, L1.enc, L1.wp, L1.y, True, d2, out, fws)
+                spc.sparse_conv_forward(d2, out, L2.wp, L2.y, False, L2.ws)
+            elif kind == "conv1":
+                L1.conv()
+            elif kind == "conv1_fused":
+                spc.sparse_conv_encode_forward(d1, L1.enc, L1.wp, L1.y, True, d2, out, fws)
+            elif kind == "encode2":
+                L2.encode(L1.y)
+    res = {}
+    for kind in ("separate", "fused", "conv1", "conv1_fused", "encode2"):
+        run(kind, nset)
+        torch.cuda.synchronize()
+        g = sets[0][1].capture(lambda: run(kind, nset), warmup=1)
+        reps = max(1, steps // nset)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[f"{kind}_us"] = e0.elapsed_time(e1) / (reps * nset) * 1e3
+        del g
+    res["encoder_saved_us"] = res["conv1_us"] + res["encode2_us"] - res["conv1_fused_us"]
+    res["chain_speedup"] = res["separate_us"] / res["fused_us"]
+    res["workload"] = "cfg4 chain: 1x7 (pad 0,3) -> ReLU -> 7x1 (pad 3,0), 8x192x17x17"
+    res["l2"] = f"back to back over {nset} buffer sets"
+    res["fused_form"] = ("layer-1 conv epilogue emits per-column output row masks; 3 launches build layer 2's "
+                         "CPO streams reading only the NZEs (no dense re-scan); bit-identical to cpo_encode")
+    return res
+
+
 # ---------------------------------------------------------------- cfg5 stack leg
 
 def run_stack(args, world, rank, dev, hbm_gbs, p_fp32, mode="best_of_three", force=None, S=None):
@@ -504,10 +595,17 @@ def run_stack(args, world, rank, dev, hbm_gbs, p_fp32, mode="best_of_three", for
             tr = tr_sparse
         t_roof += tr
         t_roof_sparse += tr_sparse
+        from paper_2104_08314_b200.bounds import space_preselect
+        rbar = float((xb != 0).mean())
         layers.append({"layer": sp["name"], "density": round(sp["density"], 4), "algo": algo,
+                       "space_preselect_vs_im2col": space_preselect(d, rbar, "im2col"),
                        "device_ms": round(lms, 4), "roofline_frac": round(tr / (lms * 1e-3), 4),
                        "nze_gflop": round(2.0 * macs / 1e9, 3)})
+    agree = sum(1 for L in layers if (L["space_preselect_vs_im2col"] == "cpo") == (L["algo"] in ("cpo", "cps")))
     res = {"workload": "cfg5 ResNet-50 3x3 stack (16 layers)", "global_batch": args.stack_batch,
+           "preselect_vs_timed_plan": {"agree": agree, "layers": len(layers),
+                                       "note": "zero-cost SI space pre-selector (CPO smaller than the im2col matrix: "
+                                               "every 3x3 layer at every density) against the timed plan"},
            "per_rank_batch": hi - lo, "n_gpus": world, "mode": mode if not force else f"forced {force}",
            "plan_source": plan_src,
            "images_per_s": args.stack_batch / (t_tot * 1e-3), "ms_per_step": t_tot, "stack_ms": t_stack,
@@ -737,6 +835,25 @@ def run_ours(args):
             del Rc
             torch.cuda.empty_cache()
 
+    extras = None
+    if not args.no_configs:
+        extras = {"fused_chain_cfg4": measure_fused_chain(dev, stream, args.config_steps, rank), "cscc": [],
+                  "stride_aware": []}
+        for name in ("cfg2", "cfg3", "cfg3s2", "cfg4a"):
+            cc = workload(name)
+            dd = cc["desc"]
+            extras["cscc"].append(measure_extra(name, dd, make_pool(cc, rank),
+                                                he_normal(dd["K"], dd["C"], dd["R"], dd["S"], cc["seed"]), dev, stream,
+                                                args.config_steps, ["cscc"]))
+            torch.cuda.empty_cache()
+        for name in ("cfg3s2", "cfg5L3", "cfg5L7", "cfg5L13"):
+            cc = workload(name)
+            dd = cc["desc"]
+            extras["stride_aware"].append(measure_extra(name, dd, make_pool(cc, rank),
+                                                        he_normal(dd["K"], dd["C"], dd["R"], dd["S"], cc["seed"]),
+                                                        dev, stream, args.config_steps, ["cpo_sa"]))
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         t, n, f = oracle_time(d, pool[:d["N"]], w, budget_s=args.cpu_budget)
@@ -802,6 +919,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "configs": rows,
+            "extras": extras,
             "stack": stack,
             "stack_cpo": stack_cpo,
             "version": spc.spc_version(),

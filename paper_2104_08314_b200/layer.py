@@ -11,6 +11,8 @@ import torch
 from . import binding as B
 
 ALGOS = {"im2col": B.SPC_ALGO_IM2COL, "cpo": B.SPC_ALGO_CPO, "cps": B.SPC_ALGO_CPS}
+# also runnable through forward(): the paper's comparison method and the stride-aware layout
+EXTRA = ("cscc", "cpo_sa")
 
 
 class SparseConvLayer:
@@ -34,6 +36,7 @@ class SparseConvLayer:
         self.wp = torch.empty_like(self.w).reshape(-1)
         B.spc_pack_weights(self.d, self.w, self.wp)
         self._lowered = None
+        self._enc_x = {}     # lazily allocated encodings of the extra algorithms
 
     @property
     def lowered(self) -> torch.Tensor:
@@ -50,7 +53,23 @@ class SparseConvLayer:
         B.sparse_conv_forward(self.d, self.enc, self.wp, self.y, self.relu, self.ws)
         return self.y
 
+    def extra_encoding(self, algo: str) -> B.Encoding:
+        if algo not in self._enc_x:
+            self._enc_x[algo] = (B.alloc_cscc_encoding(self.d, device=self.device) if algo == "cscc"
+                                 else B.alloc_strided_encoding(self.d, device=self.device))
+        return self._enc_x[algo]
+
     def forward(self, x: torch.Tensor, algo: str = "cpo") -> torch.Tensor:
+        if algo == "cscc":           # CSCC baseline (SI Alg. 5 / 6)
+            e = self.extra_encoding(algo)
+            B.cscc_encode(self.d, x, e)
+            B.cscc_conv_forward(self.d, e, self.wp, self.y, self.relu)
+            return self.y
+        if algo == "cpo_sa":         # stride-aware CPO layout (reading A32)
+            e = self.extra_encoding(algo)
+            B.cpo_encode_strided(self.d, x, e)
+            B.sparse_conv_forward(self.d, e, self.wp, self.y, self.relu, self.ws)
+            return self.y
         if algo == "im2col" or not self.sparse_ok:
             B.im2col_conv_forward(self.d, x, self.w, self.y, self.relu, self.lowered)
             return self.y
