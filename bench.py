@@ -432,7 +432,7 @@ def measure_extra(name, d, pool, w, dev, stream, steps, kinds):
     return row
 
 
-def measure_fused_chain(dev, stream, steps, rank=0):
+def measure_fused_chain(dev, stream, steps, rank=0, kinds=("separate", "fused", "conv1", "conv1_fused", "encode2")):
     """NEXT-1 on the cfg4 chain (1x7 -> ReLU -> 7x1, BASELINE.json configs[3]): layer 1's conv
     emitting layer 2's CPO encoding (sparse_conv_encode_forward) against conv + a separate
     cpo_encode of the dense intermediate; both followed by layer 2's conv.  Back to back over
@@ -476,7 +476,7 @@ def measure_fused_chain(dev, stream, steps, rank=0):
             elif kind == "encode2":
                 L2.encode(L1.y)
     res = {}
-    for kind in ("separate", "fused", "conv1", "conv1_fused", "encode2"):
+    for kind in kinds:
         run(kind, nset)
         torch.cuda.synchronize()
         g = sets[0][1].capture(lambda: run(kind, nset), warmup=1)
@@ -489,8 +489,9 @@ def measure_fused_chain(dev, stream, steps, rank=0):
         torch.cuda.synchronize()
         res[f"{kind}_us"] = e0.elapsed_time(e1) / (reps * nset) * 1e3
         del g
-    res["encoder_saved_us"] = res["conv1_us"] + res["encode2_us"] - res["conv1_fused_us"]
-    res["chain_speedup"] = res["separate_us"] / res["fused_us"]
+    if len(kinds) == 5:
+        res["encoder_saved_us"] = res["conv1_us"] + res["encode2_us"] - res["conv1_fused_us"]
+        res["chain_speedup"] = res["separate_us"] / res["fused_us"]
     res["workload"] = "cfg4 chain: 1x7 (pad 0,3) -> ReLU -> 7x1 (pad 3,0), 8x192x17x17"
     res["l2"] = f"back to back over {nset} buffer sets"
     res["fused_form"] = ("layer-1 conv epilogue emits per-column output row masks; 3 launches build layer 2's "

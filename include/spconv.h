@@ -186,7 +186,7 @@ spc_status cscc_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, co
 /* NEXT-1: the convolution emits its output ALREADY CPO-encoded
  * for the next layer.  Computes y exactly as sparse_conv_forward (ReLU if fuse_relu; y is still
  * written) and, in the same kernel's epilogue, a row bitmask per output column of the non-zero
- * outputs; three small launches then build the CPO streams of y for the layer `next` (whose
+ * outputs; one small launch then builds the CPO streams of y for the layer `next` (whose
  * input is y: next->N == N, next->C == K, next->H == Oh, next->W == Ow) from the masks, reading
  * only y's NZEs -- bit-identical to cpo_encode(next, y) (no dense re-scan of y).  `out` as for
  * cpo_encode (algo = SPC_ALGO_CPO).  ws: >= spc_fused_ws_bytes(d), zeroed once

@@ -2,6 +2,7 @@
 // Host-side validation, workspace carving, launches and the offline selector.
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -19,7 +20,8 @@ size_t sa_smem_bytes(const Geom& g);
 int sa_types(const Geom& g);
 cudaError_t launch_sa_encode(const Geom& g, const float* x, spc_encoding* e, cudaStream_t st);
 cudaError_t launch_encode_from_masks(const Geom& gn, const float* y, unsigned long long* omask, spc_encoding* e,
-                                     cudaStream_t st);
+                                     void* state, cudaStream_t st);
+size_t fe_state_bytes(const Geom& gn);
 cudaError_t launch_sa_conv(const Geom& g, const spc_encoding* e, const float* w_packed, float* y, int relu,
                            cudaStream_t st);
 cudaError_t launch_validate(const Geom& g, const spc_encoding* e, void* rec_dev, cudaStream_t st,
@@ -218,7 +220,10 @@ spc_status sparse_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, 
 size_t spc_fused_ws_bytes(const spc_conv_desc* d) {
     if (check_sparse_geometry(d) != SPC_OK) return 0;
     const spc::Geom g = spc::make_geom(*d);
-    return spc::align_up(spc::ws_layout(g).total, 256) + spc::align_up((size_t)8 * g.N * g.K * g.Ow, 256);
+    spc_conv_desc nd = *d;                     // the next layer's planes: N*K of them
+    nd.C = d->K; nd.H = g.Oh; nd.W = g.Ow;
+    return spc::align_up(spc::ws_layout(g).total, 256) + spc::align_up((size_t)8 * g.N * g.K * g.Ow, 256) +
+           spc::align_up(spc::fe_state_bytes(spc::make_geom(nd)), 256);
 }
 
 spc_status sparse_conv_encode_forward(const spc_conv_desc* d, const spc_encoding* enc, const float* w_packed,
@@ -239,11 +244,15 @@ spc_status sparse_conv_encode_forward(const spc_conv_desc* d, const spc_encoding
     if (ws_bytes < need) return fail(SPC_EINVAL, "fused workspace too small (%zu < %zu)", ws_bytes, need);
     const size_t mo = spc::align_up(spc::ws_layout(g).total, 256);
     unsigned long long* omask = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + mo);
-    s = conv_impl(d, enc, w_packed, y, fuse_relu, ws, mo, stream, omask);
+    static const int dbg = [] { const char* e = getenv("SPC_FUSE_DEBUG"); return e ? atoi(e) : 0; }();
+    s = conv_impl(d, enc, w_packed, y, fuse_relu, ws, mo, stream, dbg == 2 ? nullptr : omask);   // dev A/B: 2 = no masks
     if (s != SPC_OK) return s;
     out->algo = SPC_ALGO_CPO;
     out->geom = *next;
-    return cuda_status(spc::launch_encode_from_masks(gn, y, omask, out, (cudaStream_t)stream), "encode_from_masks");
+    if (dbg >= 1) return SPC_OK;   // dev A/B: 1 = masks only, no stream build
+    void* fstate = static_cast<unsigned char*>(ws) + mo + spc::align_up((size_t)8 * g.N * g.K * g.Ow, 256);
+    return cuda_status(spc::launch_encode_from_masks(gn, y, omask, out, fstate, (cudaStream_t)stream),
+                       "encode_from_masks");
 }
 
 spc_status im2col_conv_forward(const spc_conv_desc* d, const float* x, const float* w_kcrs, float* y,
