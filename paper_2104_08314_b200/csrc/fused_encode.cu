@@ -70,41 +70,6 @@ __device__ int fe_plane_len(const Geom& g, const int* cnt, int nnz, int* lower_o
     return plen;
 }
 
-// ptr length and NZE count of one plane straight from its column masks (no shared arrays):
-// the per-type column sums of plane_len folded into one pass over the columns
-__device__ void fe_plane_sizes(const FeArgs& a, long long plane, long long* plen_out, long long* nnz_out) {
-    const Geom& g = a.g;
-    int nnz = 0, edge[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < g.Wp; w++) {
-        const int c = __popcll(col_mask(a, plane, w));
-        nnz += c;
-        if (g.S > 1) {
-            const int t = (w < g.S - 1) ? w : ((w > g.Wp - g.S) ? (g.Wp - 1 - w) : -1);
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                if (q == t) edge[q] += c;
-        }
-    }
-    long long plen;
-    if (nnz == 0) {
-        plen = 1;                                   // NPC
-    } else if (g.S == 1) {
-        plen = 1 + g.Ow1;
-    } else {
-        plen = (g.pl == 0) ? 3 : 0;
-        int lower = (g.pl == 0) ? edge[0] : 0;
-#pragma unroll
-        for (int t = 1; t < 8; t++) {
-            if (t < max(1, g.pl) || t > g.S - 2) continue;
-            lower += edge[t];
-            plen += edge[t] ? (1 + g.Ow1) : 2;
-        }
-        plen += (nnz - lower) ? (1 + g.Ow1) : 2;
-    }
-    *plen_out = plen;
-    *nnz_out = nnz;
-}
-
 constexpr int kFeTagShift = 40;
 constexpr unsigned long long kFeValMask = (1ull << kFeTagShift) - 1;
 
