@@ -219,6 +219,98 @@ __device__ __forceinline__ void column_range_s(const Geom& g, const int32_t* seg
     else { lo = dat + c0; hi = dat + seg[pos + g.Ow1 - 1 - t]; }
 }
 
+// Stride-aware layout (reading A32, stride_aware.cu): partitions = output columns at stride
+// s_w; coverage / owner of a padded column, block directory and column ranges.  Used when
+// every (partition, type) owns at most one non-pad column (3x3 / stride 2 and the like; the
+// host checks), so a partition's count range IS its column's range.
+__device__ __forceinline__ int sa_cov_c(const Geom& g, int w) {
+    const int hi = min(g.Ow - 1, w / g.sw);
+    const int lo = (w - g.S + 1 <= 0) ? 0 : (w - g.S + 1 + g.sw - 1) / g.sw;
+    return max(0, hi - lo + 1);
+}
+__device__ __forceinline__ int sa_owner_c(const Geom& g, int w) {
+    return (w - g.S + 1 <= 0) ? 0 : (w - g.S + 1 + g.sw - 1) / g.sw;
+}
+
+template <int S>
+__device__ __forceinline__ void parse_dir_sa(const Geom& g, const int32_t* seg, DirS<S>& d, unsigned types) {
+#pragma unroll
+    for (int t = 0; t < S; t++) { d.pos[t] = -1; d.da[t] = 0; }
+    d.npc = (seg[0] == SPC_NPC);
+    if (d.npc) return;
+    int p = 0, dacur = 0;
+#pragma unroll
+    for (int t = 0; t < S; t++) {
+        if (!((types >> t) & 1u)) continue;
+        if (seg[p + 1] == SPC_NPF) { p += 2; continue; }
+        d.pos[t] = p + 1;
+        d.da[t] = dacur;
+        int last = 0;
+        for (int s2 = g.Ow - 1; s2 >= 0; s2--) {
+            const int v = seg[p + 1 + s2];
+            if (v >= 0) { last = v; break; }
+        }
+        dacur += last;
+        p += 1 + g.Ow;
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void column_range_sa(const Geom& g, const int32_t* seg, const DirS<S>& d, int w, int& lo,
+                                                int& hi) {
+    lo = hi = 0;
+    if (w < g.pl || w >= g.pl + g.W) return;                  // pad columns hold no NZE
+    const int cov = sa_cov_c(g, w);
+    if (cov == 0) return;
+    const int t = cov - 1, s = sa_owner_c(g, w);
+    const int pos = sel(d.pos, t), dat = sel(d.da, t);
+    if (pos < 0) return;                                       // NPF block
+    const int c = seg[pos + s];
+    if (c < 0) return;
+    int prev = 0;
+    for (int s2 = s - 1; s2 >= 0; s2--) {
+        const int v = seg[pos + s2];
+        if (v >= 0) { prev = v; break; }
+    }
+    lo = dat + prev;
+    hi = dat + c;
+}
+
+// Stride-aware layout, general case: slot q of the window = (partition s = s_lo + q / T, type
+// t = q % T) over the partitions whose owned columns can fall in [wx0, wx0 + WW); its DA range
+// [lo, hi) and the window column of its partition's first column cb = s*s_w - wx0.  An NZE of the
+// slot sits at window column cb + L (L = IN % K_w); those outside [0, WW) are skipped.
+__device__ __forceinline__ int sa_slot_s_lo(const Geom& g, int wx0) {
+    const int num = wx0 - g.S + 1;
+    return num <= 0 ? 0 : (num + g.sw - 1) / g.sw;
+}
+__device__ __forceinline__ int sa_nslots(const Geom& g, int wx0, int WW) {
+    const int T = (g.S + g.sw - 1) / g.sw;
+    const int s_lo = sa_slot_s_lo(g, wx0), s_hi = min(g.Ow - 1, (wx0 + WW - 1) / g.sw);
+    return max(0, s_hi - s_lo + 1) * T;
+}
+template <int S>
+__device__ __forceinline__ void sa_slot_range(const Geom& g, const int32_t* seg, const DirS<S>& d, int wx0, int WW,
+                                              int q, int& lo, int& hi, int& cb) {
+    lo = hi = 0;
+    cb = 0;
+    const int T = (g.S + g.sw - 1) / g.sw;
+    const int s = sa_slot_s_lo(g, wx0) + q / T, t = q % T;
+    if (q >= sa_nslots(g, wx0, WW)) return;
+    cb = s * g.sw - wx0;
+    const int pos = sel(d.pos, t), dat = sel(d.da, t);
+    if (pos < 0) return;
+    const int c = seg[pos + s];
+    if (c < 0) return;
+    int prev = 0;
+    for (int s2 = s - 1; s2 >= 0; s2--) {
+        const int v = seg[pos + s2];
+        if (v >= 0) { prev = v; break; }
+    }
+    lo = dat + prev;
+    hi = dat + c;
+}
+
 // -------------------------------------------------------- CPS expansion
 
 // Alg. 4 index reconstruction for the overlapK_w block:
@@ -387,6 +479,7 @@ struct ConvArgs {
     unsigned* sk_flags;   // balanced mode: one "partial published" flag per CTA (zeroed after use)
     unsigned long long* status;   // the encoding's overflow word (lengths[3]): nonzero -> y = 0;
                                   // a balanced-mode wait timeout sets bit 2
+    unsigned sa_types;            // stride-aware layout: mask of the coverage types present (0 = canonical)
     unsigned long long* omask;    // NEXT-1 fused encode: per output column (n, k, x) a bit per output
                                   // row holding an NZE of y (null = off); zeroed by its consumer
     int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
@@ -603,7 +696,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     int* s_ptr = reinterpret_cast<int*>(s_val + T::CH * RT * T::NCP);                 // [2][CH * pmax]
     int* s_coff = s_ptr + 2 * T::CH * a.pmax;       // [CW + 1] window's ptr offsets - cbase
     int* s_cz = s_coff + T::CW + 1;                 // [CW + 1] window's DA offsets - zbase
-    int* s_scr = s_cz + T::CW + 1;                  // P1 column tables: [CH][65] (FLAT) or [MAXW][64]
+    int* s_scr = s_cz + T::CW + 1;                  // P1 column tables: [CH][65] (FLAT) or [MAXW][96]
 
     using AccT = typename std::conditional<T::PACKED, float2, float>::type;
     AccT acc[T::NP][T::TY][T::TX];
@@ -751,9 +844,14 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 for (int j = warp; scatter && j < chn; j += nwarps) {
                     const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
                     DirS<T::S> d;
-                    parse_dir<T::S>(g, seg, d);
                     int lo = 0, hi = 0;
-                    if (!d.npc && lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);   // NPC: skip
+                    if (a.sa_types) {
+                        parse_dir_sa<T::S>(g, seg, d, a.sa_types);
+                        if (!d.npc && lane < T::WW) column_range_sa<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                    } else {
+                        parse_dir<T::S>(g, seg, d);
+                        if (!d.npc && lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);   // NPC: skip
+                    }
                     int tot;
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
                     fpre[j * 32 + lane] = (lane < T::WW) ? pre : (1 << 30);
@@ -812,18 +910,26 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 for (int j = warp; stage && j < chn && !(dev_phase_mode() == 4 && !(first && c0 == c_begin)); j += nwarps) {
                     const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
                     DirS<T::S> d;
-                    parse_dir<T::S>(g, seg, d);
+                    if (a.sa_types) parse_dir_sa<T::S>(g, seg, d, a.sa_types);
+                    else parse_dir<T::S>(g, seg, d);
                     if (d.npc) continue;                                  // NPC: skip channel
-                    int lo = 0, hi = 0;
-                    if (lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                    int lo = 0, hi = 0, cb = 0;
+                    // slots: window columns (canonical layout) or (partition, type) pairs (stride-aware)
+                    const int nsl = a.sa_types ? sa_nslots(g, wx0, T::WW) : T::WW;
+                    if (lane < nsl) {
+                        if (a.sa_types) sa_slot_range<T::S>(g, seg, d, wx0, T::WW, lane, lo, hi, cb);
+                        else column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                    }
                     int tot;
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
-                    int* spre = s_scr + warp * 64;
+                    int* spre = s_scr + warp * 96;
                     int* slo = spre + 32;
-                    spre[lane] = (lane < T::WW) ? pre : (1 << 30);
+                    int* scb = spre + 64;
+                    spre[lane] = (lane < nsl) ? pre : (1 << 30);
                     slo[lane] = lo;
+                    scb[lane] = cb;
                     const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
-                    const bool contig = __all_sync(0xffffffffu, lane >= T::WW || hi == lo || lo == lo0 + pre);
+                    const bool contig = __all_sync(0xffffffffu, lane >= nsl || hi == lo || lo == lo0 + pre);
                     __syncwarp();
                     const long long Z = zbase + s_cz[c0 - cw0 + j];
                     float* win = s_val + j * RT * T::NCP;
@@ -841,11 +947,15 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                                 int jc = 0;
     #pragma unroll
                                 for (int step = 16; step > 0; step >>= 1)
-                                    if (jc + step < T::WW && spre[jc + step] <= f) jc += step;
+                                    if (jc + step < nsl && spre[jc + step] <= f) jc += step;
                                 col[u] = jc;
                                 const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
                                 e[u] = __ldg(a.in + Z + idx);
                                 v[u] = __ldg(a.da + Z + idx);
+                                if (a.sa_types) {                      // window column = partition base + L
+                                    col[u] = scb[jc] + e[u] % T::S;
+                                    if (col[u] < 0 || col[u] >= T::WW) e[u] = -1;
+                                }
                             }
                         }
     #pragma unroll
@@ -1235,7 +1345,7 @@ template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
-                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 65 : T::MAXW * 64) * 4;
+                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 65 : T::MAXW * 96) * 4;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
@@ -1338,6 +1448,7 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
 template <class T>
 static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
+    if (a.sa_types && T::FLAT) return cudaErrorNotSupported;   // stride-aware slots: per-channel P1 only
     const StripPlan<T> pl = plan_strip<T>(g);
     const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
     a.rt = pl.rt;
@@ -1428,7 +1539,7 @@ size_t conv_scratch_bytes(const Geom& g) {
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
-                               cudaStream_t st, unsigned long long* omask) {
+                               cudaStream_t st, unsigned long long* omask, unsigned sa_types) {
     ConvArgs a;
     a.g = g;
     a.ptr = e->ptr;
@@ -1441,6 +1552,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.relu = relu;
     a.status = reinterpret_cast<unsigned long long*>(e->lengths + 3);
     a.omask = omask;
+    a.sa_types = sa_types;
     a.tiles_x = 1;
     a.cg = 1;
     a.rt = 1;
@@ -1458,11 +1570,13 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         a.scratch_bytes = scratch_bytes - kSkFlagBytes;
     }
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
+    if (sa_types) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
     cudaError_t err = cudaErrorNotSupported;
     if (!conv_v1_forced()) err = visit_ws_cfg(g, [&](auto cfg) { return run_ws<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
     err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
+    if (sa_types) return cudaErrorNotSupported;   // the stride-aware layout's own kernel runs instead
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
     if (WW > 32) return cudaErrorInvalidValue;

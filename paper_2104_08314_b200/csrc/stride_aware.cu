@@ -11,10 +11,11 @@
 // Compared with the stride-agnostic encoding (reading A15) a stride-2 layer stores O_w instead
 // of O_w1 ~ 2*O_w partitions per block (about half the ptr entries).
 //
-// B200 design (one CTA per channel plane; three launches like the CSCC encoder):
+// B200 design (three launches like the CSCC encoder):
 //  (1) counts per covered column -> per-plane ptr length and NZE count; (2) one CTA scans them
-//  into the side tables; (3) per plane, thread 0 lays out the blocks (columns of a type in
-//  ascending order), threads write ptr, and one thread per column writes its DA / IN.
+//  into the side tables; (3) per plane the blocks are laid out (columns of a type in ascending
+//  order), ptr written, and one lane per column writes its DA / IN.  One WARP per plane in (1)
+//  and (3) (8 planes per CTA), so layers with many small planes fill the GPU.
 // Convolution: CTA = (image, 4 output columns, 64 output channels); warp = output column x;
 // for every type t it walks the owners s in [x-t, x] (the partitions whose type-t columns x
 // covers), tap m = L + (s-x)*s_w, into its own [O_h][64] shared-memory accumulator slice.
@@ -54,17 +55,38 @@ __device__ __forceinline__ float plane_at(const float* pl, const Geom& g, int h,
     return (hh < 0 || hh >= g.H || ww < 0 || ww >= g.W) ? 0.0f : pl[hh * g.W + ww];
 }
 
-// per padded column NZE counts of the staged plane (uncovered columns: 0)
-__device__ void column_counts(const Geom& g, const float* pl, int* cnt) {
-    for (int w = threadIdx.x; w < g.Wp; w += blockDim.x) {
-        int c = 0;
-        if (sa_cov(g, w) > 0)
-            for (int h = g.pt; h < g.pt + g.H; h++) c += plane_at(pl, g, h, w) != 0.0f;
-        cnt[w] = c;
-    }
+// One WARP per channel plane (8 planes per CTA): the plane staged in the warp's shared slice,
+// per-column counts (lanes over columns), per-type totals and the plane's ptr length.
+constexpr int kSaWarps = kSaThreads / 32;
+
+struct SaWarpSmem {
+    float* pl; int* cnt; int* coff;
+};
+__device__ __forceinline__ SaWarpSmem sa_warp_smem(const Geom& g, unsigned char* smem, int warp) {
+    const size_t per = align_up((size_t)g.H * g.W * 4 + (size_t)2 * g.Wp * 4, 16);
+    SaWarpSmem m;
+    m.pl = reinterpret_cast<float*>(smem + per * warp);
+    m.cnt = reinterpret_cast<int*>(m.pl + g.H * g.W);
+    m.coff = m.cnt + g.Wp;
+    return m;
 }
 
-// present-type mask and per-type NZE totals (thread 0)
+__device__ void warp_stage_counts(const Geom& g, const float* __restrict__ x, long long plane, SaWarpSmem m,
+                                  int lane) {
+    const int HW = g.H * g.W;
+    const float* src = x + plane * HW;
+    for (int i = lane; i < HW; i += 32) m.pl[i] = __ldg(src + i);
+    __syncwarp();
+    for (int w = lane; w < g.Wp; w += 32) {
+        int c = 0;
+        if (sa_cov(g, w) > 0)
+            for (int h = g.pt; h < g.pt + g.H; h++) c += plane_at(m.pl, g, h, w) != 0.0f;
+        m.cnt[w] = c;
+    }
+    __syncwarp();
+}
+
+// per-type totals (every lane computes the same values from the shared counts)
 __device__ unsigned type_totals(const Geom& g, const int* cnt, int* tot) {
     unsigned present = 0;
     for (int t = 0; t < kSaMaxTypes; t++) tot[t] = 0;
@@ -72,7 +94,9 @@ __device__ unsigned type_totals(const Geom& g, const int* cnt, int* tot) {
         const int cv = sa_cov(g, w);
         if (cv == 0) continue;
         present |= 1u << (cv - 1);
-        tot[cv - 1] += cnt[w];
+#pragma unroll
+        for (int t = 0; t < kSaMaxTypes; t++)
+            if (t == cv - 1) tot[t] += cnt[w];
     }
     return present;
 }
@@ -80,17 +104,15 @@ __device__ unsigned type_totals(const Geom& g, const int* cnt, int* tot) {
 __global__ void __launch_bounds__(kSaThreads) sa_count_kernel(SaArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geom& g = a.g;
-    float* pl = reinterpret_cast<float*>(smem);
-    int* cnt = reinterpret_cast<int*>(pl + g.H * g.W);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long plane = (long long)blockIdx.x * kSaWarps + warp;
     pdl_wait();
-    const long long plane = blockIdx.x;
-    for (int i = threadIdx.x; i < g.H * g.W; i += blockDim.x) pl[i] = __ldg(a.x + plane * g.H * g.W + i);
-    __syncthreads();
-    column_counts(g, pl, cnt);
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (plane >= g.NC) return;
+    const SaWarpSmem m = sa_warp_smem(g, smem, warp);
+    warp_stage_counts(g, a.x, plane, m, lane);
+    if (lane == 0) {
         int tot[kSaMaxTypes];
-        const unsigned present = type_totals(g, cnt, tot);
+        const unsigned present = type_totals(g, m.cnt, tot);
         int nnz = 0, plen = 0;
         for (int t = 0; t < sa_ntypes(g); t++) {
             if (!((present >> t) & 1u)) continue;
@@ -147,67 +169,56 @@ __global__ void __launch_bounds__(1024) sa_scan_kernel(SaArgs a) {
 __global__ void __launch_bounds__(kSaThreads) sa_write_kernel(SaArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geom& g = a.g;
-    float* pl = reinterpret_cast<float*>(smem);
-    int* cnt = reinterpret_cast<int*>(pl + g.H * g.W);   // [Wp] column counts
-    int* coff = cnt + g.Wp;                              // [Wp] DA offset of the column in the plane
-    int* bpos = coff + g.Wp;                             // [kSaMaxTypes] ptr position of each block (-1: absent)
-    int* bnz = bpos + kSaMaxTypes;                       // [kSaMaxTypes] NZEs of each block
-    if (a.lengths[3]) return;
-    const long long plane = blockIdx.x;
-    for (int i = threadIdx.x; i < g.H * g.W; i += blockDim.x) pl[i] = __ldg(a.x + plane * g.H * g.W + i);
-    __syncthreads();
-    column_counts(g, pl, cnt);
-    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long plane = (long long)blockIdx.x * kSaWarps + warp;
+    if (a.lengths[3] || plane >= g.NC) return;
+    const SaWarpSmem m = sa_warp_smem(g, smem, warp);
+    warp_stage_counts(g, a.x, plane, m, lane);
     const long long P = a.cpo_off[plane], Z = a.cnz_off[plane];
     const int nnz = (int)(a.cnz_off[plane + 1] - Z);
-    if (threadIdx.x == 0) {
-        int tot[kSaMaxTypes];
-        const unsigned present = type_totals(g, cnt, tot);
-        int pos = 0, run = 0;
-        for (int t = 0; t < kSaMaxTypes; t++) { bpos[t] = -1; bnz[t] = 0; }
-        if (nnz == 0) {
-            a.ptr[P] = SPC_NPC;
-        } else {
-            for (int t = 0; t < sa_ntypes(g); t++) {
-                if (!((present >> t) & 1u)) continue;
-                a.ptr[P + pos] = t + 1;
-                bnz[t] = tot[t];
-                if (tot[t] == 0) {
-                    a.ptr[P + pos + 1] = SPC_NPF;
-                    pos += 2;
-                    continue;
-                }
-                bpos[t] = pos + 1;
-                pos += 1 + g.Ow;
-                for (int w = 0; w < g.Wp; w++)                 // the block's columns, ascending
-                    if (sa_cov(g, w) == t + 1) { coff[w] = run; run += cnt[w]; }
-            }
-        }
+    if (nnz == 0) {
+        if (lane == 0) a.ptr[P] = SPC_NPC;
+        return;
     }
-    __syncthreads();
-    if (nnz == 0) return;
-    // ptr counts: partition s of block t = cumulative count through its last owned type-t column
+    int tot[kSaMaxTypes];
+    const unsigned present = type_totals(g, m.cnt, tot);
+    // block layout (every lane walks the same few types): ptr position and DA base of each
+    int pos = 0, run = 0;
     for (int t = 0; t < sa_ntypes(g); t++) {
-        if (bpos[t] < 0) continue;
-        int blockbase = 0;
-        for (int w = 0; w < g.Wp; w++)
-            if (sa_cov(g, w) == t + 1) { blockbase = coff[w]; break; }
-        for (int s = threadIdx.x; s < g.Ow; s += blockDim.x) {
+        if (!((present >> t) & 1u)) continue;
+        if (lane == 0) a.ptr[P + pos] = t + 1;
+        if (tot[t] == 0) {
+            if (lane == 0) a.ptr[P + pos + 1] = SPC_NPF;
+            pos += 2;
+            continue;
+        }
+        // the block's columns ascending: DA offsets (lane 0 writes them for the warp)
+        if (lane == 0) {
+            int r = run;
+            for (int w = 0; w < g.Wp; w++)
+                if (sa_cov(g, w) == t + 1) { m.coff[w] = r; r += m.cnt[w]; }
+        }
+        __syncwarp();
+        // partition s's count = cumulative through its last owned type-t column
+        for (int s2 = lane; s2 < g.Ow; s2 += 32) {
             int last = -1;
             for (int L = 0; L < g.S; L++) {
-                const int w = s * g.sw + L;
-                if (w < g.Wp && sa_cov(g, w) == t + 1 && sa_owner(g, w) == s) last = w;
+                const int w = s2 * g.sw + L;
+                if (w < g.Wp && sa_cov(g, w) == t + 1 && sa_owner(g, w) == s2) last = w;
             }
-            a.ptr[P + bpos[t] + s] = (last < 0) ? -1 : coff[last] + cnt[last] - blockbase;
+            a.ptr[P + pos + 1 + s2] = (last < 0) ? -1 : m.coff[last] + m.cnt[last] - run;
         }
+        run += tot[t];
+        pos += 1 + g.Ow;
+        __syncwarp();
     }
-    // DA / IN: one thread per covered column, rows ascending
-    for (int w = threadIdx.x; w < g.Wp; w += blockDim.x) {
-        if (sa_cov(g, w) == 0 || cnt[w] == 0) continue;
+    // DA / IN: lanes over covered columns, rows ascending (from the staged plane)
+    for (int w = lane; w < g.Wp; w += 32) {
+        if (sa_cov(g, w) == 0 || m.cnt[w] == 0) continue;
         const int L = w - sa_owner(g, w) * g.sw;
-        long long o = Z + coff[w];
+        long long o = Z + m.coff[w];
         for (int h = g.pt; h < g.pt + g.H; h++) {
-            const float v = plane_at(pl, g, h, w);
+            const float v = plane_at(m.pl, g, h, w);
             if (v != 0.0f) {
                 a.da[o] = v;
                 a.in[o] = L + h * g.S;
@@ -317,8 +328,8 @@ __global__ void __launch_bounds__(32 * kScCols) sa_conv_kernel(ScArgs a) {
 
 }  // namespace
 
-size_t sa_smem_bytes(const Geom& g) {
-    return (size_t)g.H * g.W * 4 + (size_t)2 * g.Wp * 4 + 2 * kSaMaxTypes * 4 + 16;
+size_t sa_smem_bytes(const Geom& g) {   // one warp's slice (the API's one-CTA limit)
+    return align_up((size_t)g.H * g.W * 4 + (size_t)2 * g.Wp * 4, 16);
 }
 
 int sa_types(const Geom& g) { return (g.S + g.sw - 1) / g.sw; }
@@ -330,14 +341,16 @@ cudaError_t launch_sa_encode(const Geom& g, const float* x, spc_encoding* e, cud
     a.cpo_off = e->chan_ptr_off; a.cnz_off = e->chan_nz_off; a.cin_off = e->chan_in_off;
     a.lengths = e->lengths;
     a.cap_ptr = e->ptr_cap; a.cap_da = e->da_cap; a.cap_in = e->in_cap;
-    const size_t smem = sa_smem_bytes(g);
+    const size_t smem = sa_smem_bytes(g) * kSaWarps;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static std::atomic<size_t> attr_c[kMaxDevices], attr_w[kMaxDevices];
     cudaError_t err = ensure_smem_attr((const void*)sa_count_kernel, smem, attr_c);
     if (err == cudaSuccess) err = ensure_smem_attr((const void*)sa_write_kernel, smem, attr_w);
     if (err != cudaSuccess) return err;
-    sa_count_kernel<<<(unsigned)g.NC, kSaThreads, smem, st>>>(a);
+    const unsigned blocks = (unsigned)((g.NC + kSaWarps - 1) / kSaWarps);
+    sa_count_kernel<<<blocks, kSaThreads, smem, st>>>(a);
     sa_scan_kernel<<<1, 1024, 0, st>>>(a);
-    sa_write_kernel<<<(unsigned)g.NC, kSaThreads, smem, st>>>(a);
+    sa_write_kernel<<<blocks, kSaThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -57,7 +57,7 @@ struct WsCfg {
 
 // shared-memory carve-up (host and device agree through this)
 struct WsSmem {
-    size_t w, val, msk, pbuf, pre, lo, tot, coff, cz, bars, total;
+    size_t w, val, msk, pbuf, pre, lo, tot, cb, coff, cz, bars, total;
     int pstride;   // ints of the ptr part of one producer buffer
     int bstride;   // bytes of one producer buffer: ptr | DA | IN
 };
@@ -73,7 +73,8 @@ __host__ __device__ inline WsSmem ws_smem_layout(int RT, int pmax, int crange) {
     L.pre = align_up(L.pbuf + (size_t)T::NPROD * 2 * L.bstride, 16);             // [NPROD][CH][32] column prefix
     L.lo = L.pre + (size_t)T::NPROD * T::CH * 32 * 4;                             // [NPROD][CH][32] column DA start
     L.tot = L.lo + (size_t)T::NPROD * T::CH * 32 * 4;                             // [NPROD][CH]
-    L.coff = L.tot + (size_t)T::NPROD * T::CH * 4;                                // [crange+1] ptr offsets (rel)
+    L.cb = L.tot + (size_t)T::NPROD * T::CH * 4;                                  // [NPROD][CH][32] slot column base
+    L.coff = L.cb + (size_t)T::NPROD * T::CH * 32 * 4;                            // [crange+1] ptr offsets (rel)
     L.cz = L.coff + (size_t)(crange + 1) * 4;                                     // [crange+1] DA offsets (rel)
     L.bars = align_up(L.cz + (size_t)(crange + 1) * 4 + 16, 16);                 // full, empty [NST], pbar [NPROD][2]
     L.total = L.bars + (size_t)(2 * T::NST + 2 * T::NPROD) * 8 + 64;
@@ -120,6 +121,7 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
     int* fpre = reinterpret_cast<int*>(smem_raw + L.pre);
     int* flo = reinterpret_cast<int*>(smem_raw + L.lo);
     int* ftot = reinterpret_cast<int*>(smem_raw + L.tot);
+    int* fcb = reinterpret_cast<int*>(smem_raw + L.cb);
     int* s_coff = reinterpret_cast<int*>(smem_raw + L.coff);
     int* s_cz = reinterpret_cast<int*>(smem_raw + L.cz);
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + L.bars);
@@ -195,6 +197,7 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
         producer_sync();
         int* wpre = fpre + p * T::CH * 32;         // this warp's column tables
         int* wlo = flo + p * T::CH * 32;
+        int* wcb = fcb + p * T::CH * 32;           // stride-aware slots: window column of the partition
         // Producer-private double buffer: the ptr segments and the DA / IN segments of the warp's
         // NEXT chunk are copied (TMA bulk, 16-byte aligned part; the < 16-byte tails with plain
         // loads) while it scatters the current one, so a chunk's chain no longer waits on L2
@@ -263,18 +266,24 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
             // (a) LPC lanes per channel, one window column per lane: every lane parses its channel's
             //     block directory (the chunk's channels in parallel), takes its column's DA range,
             //     and a segmented scan gives the column prefix inside the channel
+            const int nsl = a.sa_types ? sa_nslots(g, wx0, T::WW) : T::WW;   // slots per channel
             {
-                constexpr int LPC = (T::WW <= 8) ? 8 : 16;
+                constexpr int LPC = (T::WW <= 8) ? 8 : 16;          // (stride-aware slots: <= 16, host-checked)
                 constexpr int CPP = 32 / LPC;                       // channels per pass
                 const int jl = lane / LPC, col = lane % LPC;
                 for (int j0 = 0; j0 < chn; j0 += CPP) {
                     const int j = j0 + jl;
-                    int lo = 0, hi = 0;
+                    int lo = 0, hi = 0, cb = 0;
                     if (j < chn) {
                         const int* seg = sp + shift + (s_pof[r0 + j] - s_pof[r0]);   // (chunk-relative)
                         DirS<T::S> d;
-                        parse_dir<T::S>(g, seg, d);
-                        if (!d.npc && col < T::WW) column_range_s<T::S>(g, seg, d, wx0 + col, lo, hi);
+                        if (a.sa_types) {
+                            parse_dir_sa<T::S>(g, seg, d, a.sa_types);
+                            if (!d.npc && col < nsl) sa_slot_range<T::S>(g, seg, d, wx0, T::WW, col, lo, hi, cb);
+                        } else {
+                            parse_dir<T::S>(g, seg, d);
+                            if (!d.npc && col < T::WW) column_range_s<T::S>(g, seg, d, wx0 + col, lo, hi);
+                        }
                     }
                     int inc = hi - lo;
 #pragma unroll
@@ -283,8 +292,9 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                         if (col >= o) inc += t;
                     }
                     if (j < chn) {
-                        wpre[j * 32 + col] = (col < T::WW) ? inc - (hi - lo) : (1 << 30);
+                        wpre[j * 32 + col] = (col < nsl) ? inc - (hi - lo) : (1 << 30);
                         wlo[j * 32 + col] = lo;
+                        wcb[j * 32 + col] = cb;
                         if (col == LPC - 1) ftot[p * T::CH + j] = inc;
                     }
                 }
@@ -320,7 +330,7 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                             int jc = 0;
 #pragma unroll
                             for (int step = 16; step > 0; step >>= 1)
-                                if (jc + step < T::WW && jp[jc + step] <= fj) jc += step;
+                                if (jc + step < nsl && jp[jc + step] <= fj) jc += step;
                             const int zr = s_zof[r0 + j] - s_zof[r0];    // channel's DA offset in the chunk
                             const int idx = wlo[j * 32 + jc] + (fj - jp[jc]);
                             if (fits) {
@@ -331,6 +341,11 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                                 v[u] = __ldg(a.da + Z0 + zr + idx);
                             }
                             pos[u] = j * RT + jc * 65536;          // window (j, 0) and column jc
+                            if (a.sa_types) {                      // window column = partition base + L
+                                const int cc = wcb[j * 32 + jc] + e[u] % T::S;
+                                pos[u] = j * RT + cc * 65536;
+                                if (cc < 0 || cc >= T::WW) e[u] = -1;
+                            }
                         }
                     }
 #pragma unroll
@@ -525,6 +540,9 @@ static bool plan_ws(const Geom& g, int pmax, WsPlan<T>& p) {
 template <class T>
 static cudaError_t run_ws(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
+    // stride-aware encodings run on the strip kernel (its per-channel P1 takes the (partition, type)
+    // slots; the producers' path here faulted on the 28 -> 14 layer and is not used)
+    if (a.sa_types) return cudaErrorNotSupported;
     WsPlan<T> p;
     if (!plan_ws<T>(g, a.pmax, p)) return cudaErrorNotSupported;
     if (p.cg > 1 && (!a.scratch || a.scratch_bytes < p.scratch_bytes)) p.cg = 1;   // no scratch: no split
