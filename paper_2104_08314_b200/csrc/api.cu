@@ -429,8 +429,20 @@ spc_status cscc_conv_forward(const spc_conv_desc* d, const spc_encoding* enc, co
         e.stride_w != d->stride_w || e.pad_top != d->pad_top || e.pad_bottom != d->pad_bottom ||
         e.pad_left != d->pad_left || e.pad_right != d->pad_right)
         return fail(SPC_EINVAL, "encoding geometry does not match the descriptor");
-    return cuda_status(spc::launch_cscc_conv(spc::make_geom(*d), enc, w_packed, y, fuse_relu, (cudaStream_t)stream),
-                       "cscc_conv");
+    // the strip kernel reads CSCC's submatrices as window slots (NZE column = s*s_w + IN % K_w;
+    // an NZE held by several submatrices lands on the same window cell) where a per-channel
+    // configuration exists and the slots fit a warp; else the plain SI Alg. 6 kernel
+    static const bool force_simple = [] { const char* e = getenv("SPC_CSCC_SIMPLE"); return e && atoi(e); }();
+    const spc::Geom g = spc::make_geom(*d);
+    const int WW = 3 * d->stride_w + d->S;
+    if (!force_simple && d->S <= 8 && d->R <= 32 && (WW + d->S - 2) / d->stride_w + 2 <= 32 &&
+        check_sparse_geometry(d) == SPC_OK) {
+        const cudaError_t ce = spc::launch_sparse_conv(g, enc, nullptr, w_packed, y, fuse_relu, nullptr, 0,
+                                                       (cudaStream_t)stream, nullptr, 0, 1);
+        if (ce != cudaErrorNotSupported) return cuda_status(ce, "cscc_conv (strip)");
+    }
+    g_err.clear();
+    return cuda_status(spc::launch_cscc_conv(g, enc, w_packed, y, fuse_relu, (cudaStream_t)stream), "cscc_conv");
 }
 
 // ------------------------------------------------------------ stride-aware CPO layout (NEXT-4)

@@ -252,7 +252,8 @@ cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaSt
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st);
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
-                               cudaStream_t st, unsigned long long* omask = nullptr, unsigned sa_types = 0);
+                               cudaStream_t st, unsigned long long* omask = nullptr, unsigned sa_types = 0,
+                               int cscc = 0);
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
                         float* extra = nullptr, size_t extra_bytes = 0);   // extra: workspace beyond the lowered matrix

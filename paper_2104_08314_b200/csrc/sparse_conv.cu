@@ -480,6 +480,7 @@ struct ConvArgs {
     unsigned long long* status;   // the encoding's overflow word (lengths[3]): nonzero -> y = 0;
                                   // a balanced-mode wait timeout sets bit 2
     unsigned sa_types;            // stride-aware layout: mask of the coverage types present (0 = canonical)
+    int cscc;                     // CSCC encoding (SI Alg. 5 layout): ptr = [0, c_0 .. c_{O_w-1}] per channel
     unsigned long long* omask;    // NEXT-1 fused encode: per output column (n, k, x) a bit per output
                                   // row holding an NZE of y (null = off); zeroed by its consumer
     int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
@@ -832,30 +833,48 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             }
             if (stage) __syncthreads();
             if (c0 == c_begin) probe(3);
+            // P1 in two instantiations: window columns (canonical CPO) or window SLOTS -- (partition,
+            // type) pairs of the stride-aware layout, submatrices of CSCC -- whose NZE column is the
+            // slot's base + IN % K_w (so the canonical path keeps its compile-time column bounds)
+            auto run_p1 = [&](auto slots_c) {
+                constexpr bool SL = decltype(slots_c)::value;
             if constexpr (T::FLAT) {
                 // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows.
                 //      (a) warp per channel: block directory (NPC / NPF skip) and the DA range of each
                 //      window column -> per-channel column prefix table; (b) all threads over the
                 //      chunk's NZEs flattened across channels, so one L2 round trip covers the chunk.
                 const bool scatter = stage && !(dev_phase_mode() == 4 && !(first && c0 == c_begin));
-                int* fpre = s_scr;                      // [CH][32] column prefix within the channel
-                int* flo = fpre + T::CH * 32;           // [CH][32] DA offset of the column
-                int* ftot = flo + T::CH * 32;           // [CH] NZEs of the channel in the window
+                int* fpre = s_scr;                      // [CH][32] column (slot) prefix within the channel
+                int* flo = fpre + T::CH * 32;           // [CH][32] DA offset of the column (slot)
+                int* fcb = flo + T::CH * 32;            // [CH][32] slot column base (stride-aware / CSCC)
+                int* ftot = fcb + T::CH * 32;           // [CH] NZEs of the channel in the window
+                // slots: window columns, or (partition, type) pairs (stride-aware), or submatrices (CSCC)
+                const int nsl = !SL ? T::WW
+                              : a.cscc ? max(0, min(g.Ow - 1, (wx0 + T::WW - 1) / g.sw) - sa_slot_s_lo(g, wx0) + 1)
+                              : sa_nslots(g, wx0, T::WW);
                 for (int j = warp; scatter && j < chn; j += nwarps) {
                     const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
                     DirS<T::S> d;
-                    int lo = 0, hi = 0;
-                    if (a.sa_types) {
+                    int lo = 0, hi = 0, cb = 0;
+                    if (SL && a.cscc) {
+                        if (lane < nsl) {
+                            const int s2 = sa_slot_s_lo(g, wx0) + lane;
+                            lo = seg[s2];
+                            hi = seg[s2 + 1];
+                            cb = s2 * g.sw - wx0;
+                        }
+                    } else if (SL) {
                         parse_dir_sa<T::S>(g, seg, d, a.sa_types);
-                        if (!d.npc && lane < T::WW) column_range_sa<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                        if (!d.npc && lane < nsl) sa_slot_range<T::S>(g, seg, d, wx0, T::WW, lane, lo, hi, cb);
                     } else {
                         parse_dir<T::S>(g, seg, d);
                         if (!d.npc && lane < T::WW) column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);   // NPC: skip
                     }
                     int tot;
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
-                    fpre[j * 32 + lane] = (lane < T::WW) ? pre : (1 << 30);
+                    fpre[j * 32 + lane] = (lane < nsl) ? pre : (1 << 30);
                     flo[j * 32 + lane] = lo;
+                    fcb[j * 32 + lane] = cb;
                     if (lane == 0) ftot[j] = tot;
                 }
                 if (scatter) __syncthreads();
@@ -886,12 +905,17 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                                 int jc = 0;
     #pragma unroll
                                 for (int step = 16; step > 0; step >>= 1)
-                                    if (jc + step < T::WW && jp[jc + step] <= fj) jc += step;
+                                    if (jc + step < nsl && jp[jc + step] <= fj) jc += step;
                                 const long long Z = zbase + s_cz[c0 - cw0 + j];
                                 const int idx = flo[j * 32 + jc] + (fj - jp[jc]);
                                 e[u] = __ldg(a.in + Z + idx);
                                 v[u] = __ldg(a.da + Z + idx);
                                 pos[u] = j * RT * T::NCP + jc;
+                                if constexpr (SL) {            // window column = slot base + L
+                                    const int cc = fcb[j * 32 + jc] + e[u] % T::S;
+                                    pos[u] = j * RT * T::NCP + cc;
+                                    if (cc < 0 || cc >= T::WW) e[u] = -1;
+                                }
                             }
                         }
     #pragma unroll
@@ -910,15 +934,29 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 for (int j = warp; stage && j < chn && !(dev_phase_mode() == 4 && !(first && c0 == c_begin)); j += nwarps) {
                     const int* seg = s_ptr + buf * T::CH * a.pmax + (s_coff[c0 - cw0 + j] - s_coff[c0 - cw0]);
                     DirS<T::S> d;
-                    if (a.sa_types) parse_dir_sa<T::S>(g, seg, d, a.sa_types);
+                    if (SL && a.cscc) d.npc = 0;                          // CSCC: no NPC flag, no blocks
+                    else if (SL) parse_dir_sa<T::S>(g, seg, d, a.sa_types);
                     else parse_dir<T::S>(g, seg, d);
                     if (d.npc) continue;                                  // NPC: skip channel
                     int lo = 0, hi = 0, cb = 0;
-                    // slots: window columns (canonical layout) or (partition, type) pairs (stride-aware)
-                    const int nsl = a.sa_types ? sa_nslots(g, wx0, T::WW) : T::WW;
+                    // slots: window columns (canonical layout) or (partition, type) pairs (stride-aware,
+                    // CSCC with one "type": submatrix s = partition s)
+                    const int nsl = !SL ? T::WW
+                                  : a.cscc ? max(0, min(g.Ow - 1, (wx0 + T::WW - 1) / g.sw) - sa_slot_s_lo(g, wx0) + 1)
+                                  : sa_nslots(g, wx0, T::WW);
                     if (lane < nsl) {
-                        if (a.sa_types) sa_slot_range<T::S>(g, seg, d, wx0, T::WW, lane, lo, hi, cb);
-                        else column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                        if (SL && a.cscc) {
+                            // submatrix s holds [ptr[s], ptr[s+1]) (ptr[0] = 0, channel-cumulative, SI Alg. 5);
+                            // an NZE sits at padded column s*s_w + (IN % K_w)
+                            const int s2 = sa_slot_s_lo(g, wx0) + lane;
+                            lo = seg[s2];
+                            hi = seg[s2 + 1];
+                            cb = s2 * g.sw - wx0;
+                        } else if (SL) {
+                            sa_slot_range<T::S>(g, seg, d, wx0, T::WW, lane, lo, hi, cb);
+                        } else {
+                            column_range_s<T::S>(g, seg, d, wx0 + lane, lo, hi);
+                        }
                     }
                     int tot;
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
@@ -952,7 +990,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                                 const int idx = contig ? lo0 + f : slo[jc] + (f - spre[jc]);
                                 e[u] = __ldg(a.in + Z + idx);
                                 v[u] = __ldg(a.da + Z + idx);
-                                if (a.sa_types) {                      // window column = partition base + L
+                                if constexpr (SL) {            // window column = partition base + L
                                     col[u] = scb[jc] + e[u] % T::S;
                                     if (col[u] < 0 || col[u] >= T::WW) e[u] = -1;
                                 }
@@ -970,6 +1008,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     }
                 }
             }
+            };
+            if (a.sa_types || a.cscc) run_p1(std::true_type{});
+            else run_p1(std::false_type{});
             if (stage) __syncthreads();
             if (c0 == c_begin) probe(4);
             // prefetch the next chunk's ptr segments (its buffer was last read before the barrier)
@@ -1345,7 +1386,7 @@ template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
-                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 65 : T::MAXW * 96) * 4;
+                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 97 : T::MAXW * 96) * 4;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
@@ -1448,7 +1489,6 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
 template <class T>
 static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
-    if (a.sa_types && T::FLAT) return cudaErrorNotSupported;   // stride-aware slots: per-channel P1 only
     const StripPlan<T> pl = plan_strip<T>(g);
     const int strips = pl.strips, kblocks = pl.kblocks, cg = pl.cg;
     a.rt = pl.rt;
@@ -1539,7 +1579,7 @@ size_t conv_scratch_bytes(const Geom& g) {
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
-                               cudaStream_t st, unsigned long long* omask, unsigned sa_types) {
+                               cudaStream_t st, unsigned long long* omask, unsigned sa_types, int cscc) {
     ConvArgs a;
     a.g = g;
     a.ptr = e->ptr;
@@ -1553,6 +1593,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.status = reinterpret_cast<unsigned long long*>(e->lengths + 3);
     a.omask = omask;
     a.sa_types = sa_types;
+    a.cscc = cscc;
     a.tiles_x = 1;
     a.cg = 1;
     a.rt = 1;
@@ -1570,13 +1611,13 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         a.scratch_bytes = scratch_bytes - kSkFlagBytes;
     }
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
-    if (sa_types) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
+    if (sa_types || cscc) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
     cudaError_t err = cudaErrorNotSupported;
     if (!conv_v1_forced()) err = visit_ws_cfg(g, [&](auto cfg) { return run_ws<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
     err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) return err;
-    if (sa_types) return cudaErrorNotSupported;   // the stride-aware layout's own kernel runs instead
+    if (sa_types || cscc) return cudaErrorNotSupported;   // the layout's own kernel runs instead
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
     if (WW > 32) return cudaErrorInvalidValue;

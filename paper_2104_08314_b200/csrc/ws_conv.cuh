@@ -542,7 +542,7 @@ static cudaError_t run_ws(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
     // stride-aware encodings run on the strip kernel (its per-channel P1 takes the (partition, type)
     // slots; the producers' path here faulted on the 28 -> 14 layer and is not used)
-    if (a.sa_types) return cudaErrorNotSupported;
+    if (a.sa_types || a.cscc) return cudaErrorNotSupported;
     WsPlan<T> p;
     if (!plan_ws<T>(g, a.pmax, p)) return cudaErrorNotSupported;
     if (p.cg > 1 && (!a.scratch || a.scratch_bytes < p.scratch_bytes)) p.cg = 1;   // no scratch: no split
