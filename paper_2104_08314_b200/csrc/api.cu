@@ -186,33 +186,19 @@ spc_status conv_impl(const spc_conv_desc* d, const spc_encoding* enc, const floa
         if (e.stride_w != d->stride_w) return fail(SPC_EINVAL, "stride-aware encoding made for another stride");
         if ((size_t)4 * g.Oh * 32 * 8 > 227 * 1024) return fail(SPC_EUNSUPPORTED, "output too tall");
         if (omask) return fail(SPC_EUNSUPPORTED, "fused encode: CPO / CPS input encodings only");
-        // the strip / warp-specialised kernels read the layout when every (partition, type) owns at
-        // most one non-pad column (its count range is then the column's range); else the layout's
-        // own kernel
+        // the coverage types present in the padded row (which (partition, type) slots exist)
         unsigned types = 0;
-        bool one_col = true;
-        {
-            std::vector<int> own((size_t)g.Ow * 8, 0);
-            for (int w = g.pl; w < g.pl + g.W; w++) {
-                int cov = 0, owner = -1;
-                for (int s2 = 0; s2 < g.Ow; s2++)
-                    if (s2 * g.sw <= w && w < s2 * g.sw + g.S) { cov++; if (owner < 0) owner = s2; }
-                if (!cov) continue;
-                if (++own[(size_t)owner * 8 + (cov - 1)] > 1) one_col = false;
-            }
-            for (int w = 0; w < g.Wp; w++) {
-                int cov = 0;
-                for (int s2 = 0; s2 < g.Ow; s2++)
-                    if (s2 * g.sw <= w && w < s2 * g.sw + g.S) cov++;
-                if (cov) types |= 1u << (cov - 1);
-            }
+        for (int w = 0; w < g.Wp; w++) {
+            int cov = 0;
+            for (int s2 = 0; s2 < g.Ow; s2++)
+                if (s2 * g.sw <= w && w < s2 * g.sw + g.S) cov++;
+            if (cov) types |= 1u << (cov - 1);
         }
         static const bool force_simple = [] { const char* e = getenv("SPC_SA_SIMPLE"); return e && atoi(e); }();
         // the strip / ws producers address (partition, type) slots of the window: <= 32 per channel
         const int T = (d->S + d->stride_w - 1) / d->stride_w;
         const int WW = 3 * d->stride_w + d->S;                      // window columns of a 4-output strip
         const bool slots_ok = ((WW + d->S - 2) / d->stride_w + 2) * T <= (WW <= 8 ? 8 : 16);
-        (void)one_col;
         if (slots_ok && !force_simple) {
             float* scratch = nullptr;
             size_t scratch_bytes = 0;
