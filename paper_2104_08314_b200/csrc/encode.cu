@@ -137,7 +137,7 @@ __device__ __forceinline__ void plane_lengths(const Geom& g, const int* wc, int 
 }
 
 template <bool CPS>
-__global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
     const Geom& g = a.g;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ long long s_red[kEncWarps][3];
@@ -583,26 +583,35 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncArgs a) {
                 }
             }
         }
-        // ---- 7c. CPS IN of the overlapK_w columns: warp per column, lane per set4 group
+        // ---- 7c. CPS IN of the overlapK_w columns: lane per set4 group, G lanes per column
+        //          (G = 8 / 16 / 32 by the padded height: short columns share a warp)
         if (CPS) {
-            for (int it = warp; it < np * Wp; it += kEncWarps) {
+            const int NG = 8 * NW;                          // set4 groups per padded column
+            const int G = (NG <= 8) ? 8 : (NG <= 16) ? 16 : 32;
+            const int CPW = 32 / G, sub = lane / G, sl = lane % G;
+            for (int it0 = warp * CPW; it0 < np * Wp; it0 += kEncWarps * CPW) {
+                const int it = it0 + sub;
                 const int p = it / Wp, w = it % Wp;
-                if (!is_middle(g, w) || cnt[it] == 0 || !poff[4 * p + 3]) continue;
-                const int L = local_of(g, w);
-                int32_t* ii = a.in + poff[4 * p + 2] + inb[it];
-                const unsigned* mw = msk + it * NW;
+                const bool act = it < np * Wp && is_middle(g, w) && cnt[it] != 0 && poff[4 * p + 3];
+                const int L = act ? local_of(g, w) : 0;
+                int32_t* ii = act ? a.in + poff[4 * p + 2] + inb[it] : nullptr;
+                const unsigned* mw = msk + (act ? it : 0) * NW;
                 int irun = 0;
-                for (int g0 = 0; g0 < 8 * NW; g0 += 32) {
-                    const int grp = g0 + lane;           // rows 4*grp .. 4*grp+3
+                for (int g0 = 0; g0 < NG; g0 += G) {
+                    const int grp = g0 + sl;                // rows 4*grp .. 4*grp+3
                     unsigned nib = 0;
-                    if (grp < 8 * NW) nib = (mw[grp >> 3] >> (4 * (grp & 7))) & 0xFu;
+                    if (act && grp < NG) nib = (mw[grp >> 3] >> (4 * (grp & 7))) & 0xFu;
                     const int k = __popc(nib);
                     const int e = k >= 3 ? 2 : k;
-                    int te;
-                    const int eo = warp_exclusive_scan(e, &te);
+                    int inc = e;                            // scan inside the column's G lanes
+                    for (int o = 1; o < G; o <<= 1) {
+                        const int t = __shfl_up_sync(0xffffffffu, inc, o, G);
+                        if (sl >= o) inc += t;
+                    }
+                    const int te = __shfl_sync(0xffffffffu, inc, G - 1, G);
                     if (k) {
                         const int row0 = 4 * grp;
-                        int32_t* o = ii + irun + eo;
+                        int32_t* o = ii + irun + (inc - e);
                         if (k >= 3) {
                             o[0] = L + (row0 + __ffs(nib) - 1) * g.S;  // first NZE index (A9)
                             o[1] = (int32_t)nib;                         // pattern, bit b = row b (A12)

@@ -430,9 +430,43 @@ __global__ void __launch_bounds__(256) cps_expand_kernel(Geom g, const int32_t* 
     if (q0 < q1) cps_segment<true>(in, Q, q0, q1, nin, carry, g.S, out, Z + base);
 }
 
+// Many small channels (14x14 / 7x7 planes, or batches of thousands of channels): one warp per
+// channel, 8 channels per CTA -- the overlapK_w block of such a channel is a few dozen entries,
+// so splitting it over 8 warps (above) only added a CTA barrier and a count pass per channel.
+__global__ void __launch_bounds__(256) cps_expand_warp_kernel(Geom g, const int32_t* __restrict__ ptr,
+                                                              const int32_t* __restrict__ in,
+                                                              const int64_t* __restrict__ cpo_off,
+                                                              const int64_t* __restrict__ cnz_off,
+                                                              const int64_t* __restrict__ cin_off,
+                                                              int32_t* __restrict__ out,
+                                                              const unsigned long long* status) {
+    const int lane = threadIdx.x & 31;
+    const long long nc = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+    pdl_wait();
+    pdl_trigger();
+    if (nc >= g.NC) return;
+    if (*reinterpret_cast<volatile const unsigned long long*>(status) != 0ull) return;   // flagged encoding
+    const long long Z = cnz_off[nc], Q = cin_off[nc];
+    const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q);
+    if (nnz == 0) return;
+    const int e0 = (lane < nin) ? __ldg(in + Q + lane) : 0;   // in flight during the directory parse
+    int dmid = nnz;
+    if (g.S > 1) {
+        ChanDir d;
+        parse_channel(g, ptr, cpo_off[nc], d);
+        dmid = (d.pos[g.S - 1] >= 0) ? d.da[g.S - 1] : nnz;
+    }
+    if (lane < dmid) out[Z + lane] = e0;
+    for (int r = 32 + lane; r < dmid; r += 32) out[Z + r] = __ldg(in + Q + r);
+    if (dmid < nnz) cps_segment<true>(in, Q, dmid, nin, nin, false, g.S, out, Z + dmid);
+}
+
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st) {
+    static const int force = [] { const char* v = getenv("SPC_CPS_EXPAND"); return v ? atoi(v) : 0; }();
+    const bool per_warp = force ? force == 1 : (g.H * g.W <= 1024 || g.NC >= 4096);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)g.NC);     // one CTA (8 warp segments) per channel
+    cfg.gridDim = dim3(per_warp ? (unsigned)((g.NC + 7) / 8)    // one warp per channel
+                                : (unsigned)g.NC);              // one CTA (8 warp segments) per channel
     cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -440,7 +474,8 @@ cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, cps_expand_kernel, g, (const int32_t*)e->ptr, (const int32_t*)e->in,
+    return cudaLaunchKernelEx(&cfg, per_warp ? cps_expand_warp_kernel : cps_expand_kernel, g, (const int32_t*)e->ptr,
+                              (const int32_t*)e->in,
                               (const int64_t*)e->chan_ptr_off, (const int64_t*)e->chan_nz_off,
                               (const int64_t*)e->chan_in_off, in_cpo,
                               (const unsigned long long*)(e->lengths + 3));

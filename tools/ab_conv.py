@@ -23,6 +23,7 @@ def main():
     ap.add_argument("names", nargs="+")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--rho", type=float, default=None)
+    ap.add_argument("--cps", action="store_true", help="also time the CPS step")
     ap.add_argument("--check", action="store_true", help="compare y against torch conv2d (fp64) on set 0")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -36,7 +37,7 @@ def main():
         d = c["desc"]
         pool = bench.make_pool(c)
         w = he_normal(d["K"], d["C"], d["R"], d["S"], c["seed"])
-        row, R = bench.measure_layer(name, d, pool, w, dev, stream, args.steps, hbm, p32, im2col=False, cps=False)
+        row, R = bench.measure_layer(name, d, pool, w, dev, stream, args.steps, hbm, p32, im2col=False, cps=args.cps)
         if args.check:
             L = R.layers[0]
             L.forward(R.xs[0], "cpo")
