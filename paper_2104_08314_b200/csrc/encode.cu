@@ -658,6 +658,8 @@ EncPlan plan_encode(const Geom& g) {
         const long long rounds = (g.NC + slots * pmax - 1) / (slots * pmax);
         P = (g.NC + slots * rounds - 1) / (slots * rounds);
     }
+    static const int force_p = [] { const char* v = getenv("SPC_ENC_P"); return v ? atoi(v) : 0; }();
+    if (force_p > 0 && enc_smem_layout(g, force_p).total <= b1) P = force_p;   // development A/B
     pl.P = (int)std::max(1ll, P);
     pl.ntiles = (int)((g.NC + pl.P - 1) / pl.P);
     pl.smem = enc_smem_layout(g, pl.P).total;

@@ -81,3 +81,32 @@ def test_preselector_routes_by_the_bound():
     q = cscc_q_bound(d)
     assert space_preselect(d, 0.0, "cscc", max(0.0, q) + 0.05) == "cpo"
     assert space_preselect(d, 1.0, "cscc", 0.0) == "cscc"
+
+
+MEC_SHAPES = [layer_desc(1, 4, 7, 7, 4, 3, 3, 1, 1, 0, 0, 0, 0), layer_desc(1, 3, 20, 5, 4, 3, 3, 1, 1, 0, 0, 0, 0),
+              layer_desc(2, 2, 30, 6, 4, 1, 3, 1, 1, 0, 0, 0, 0)]
+
+
+@pytest.mark.parametrize("i", range(len(MEC_SHAPES)))
+def test_mec_bound_on_real_encodings(oracle_mod, i):
+    """P(rho) against MEC on real oracle encodings: S_MEC of Eq. 11 equals the
+    size of the MEC lowered matrix the oracle builds (SI Eq. 11 matrix, VALID); maps just below the
+    bound encode no larger than S_MEC, maps just above it larger (worst case: no NPC / NPF)."""
+    d = MEC_SHAPES[i]
+    rb = sizes.p_bound_mec(d)
+    assert 0.0 < rb < 1.0
+    s_mec = sizes.S_mec(d)
+    hw = d["H"] * d["W"]
+    for target, expect_le in ((rb - 0.03, True), (min(1.0, rb + 0.03), False)):
+        rng = np.random.default_rng(i)
+        x = np.zeros((d["N"], d["C"], d["H"], d["W"]), np.float32)
+        k = int(round(target * hw))
+        for n in range(d["N"]):
+            for c in range(d["C"]):
+                x[n, c].flat[rng.permutation(hw)[:k]] = 1.0
+        assert oracle_mod.mec_lower(d, x).size == s_mec
+        enc = oracle_mod.encode(d, x)
+        npc, npf = oracle_mod.count_flags(enc["ptr"])
+        assert not npc and not npf
+        s_cpo = len(enc["ptr"]) + len(enc["da"]) + len(enc["inn"])
+        assert (s_cpo <= s_mec) == expect_le, (d, target, s_cpo, s_mec)
