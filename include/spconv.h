@@ -159,9 +159,14 @@ spc_status sparse_conv_forward(const spc_conv_desc *d, const spc_encoding *enc, 
  * algo = SPC_ALGO_CPO_SA; sparse_conv_forward accepts it (the encoding's stride_w must equal
  * the descriptor's).  Capacities: ptr <= N*C*max(1, ceil(K_w/s_w)*(1+O_w)), da = in <= N*C*H*W. */
 spc_status spc_strided_capacity(const spc_conv_desc *d, int64_t *ptr_cap, int64_t *da_cap, int64_t *in_cap);
-/* Three launches (counts, scan, writes); lengths[3] = 1 (nothing written) when a capacity is
- * too small.  SPC_EUNSUPPORTED: pointwise, K_w > 8, or a plane too large for one CTA. */
-spc_status cpo_encode_strided(const spc_conv_desc *d, const float *x, spc_encoding *out, void *stream);
+/* ws (>= ws_bytes from spc_encode_capacity, zeroed once, shareable with cpo_encode on the same
+ * stream) and the canonical preconditions of cpo_encode: one launch -- the canonical encoder's
+ * kernel with this layout's column order and ptr blocks (capacity overflow as in cpo_encode).
+ * ws = NULL (or a geometry outside those preconditions): three launches (counts, scan, writes);
+ * lengths[3] = 1 (nothing written) when a capacity is too small.  The streams are identical.
+ * SPC_EUNSUPPORTED: pointwise, K_w > 8, or a plane too large for one CTA. */
+spc_status cpo_encode_strided(const spc_conv_desc *d, const float *x, spc_encoding *out, void *ws, size_t ws_bytes,
+                              void *stream);
 
 /* ---- CSCC, the paper's comparison method.
  * Encoding = SI Alg. 5, the paper's simplification of the CSCC encoder

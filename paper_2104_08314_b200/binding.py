@@ -73,7 +73,7 @@ _sigs = {
     "spc_cscc_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "spc_space_bound": [_D, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
     "spc_strided_capacity": [_D, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
-    "cpo_encode_strided": [_D, _vp, _E, _vp],
+    "cpo_encode_strided": [_D, _vp, _E, _vp, _sz, _vp],
     "sparse_conv_encode_forward": [_D, _E, _vp, _vp, _i32, _D, _E, _vp, _sz, _vp],
     "spc_cscc_q_bound": [_D, ctypes.POINTER(ctypes.c_double)],
     "spc_space_preselect": [_D, _i32, ctypes.c_double, ctypes.c_double, ctypes.POINTER(_i32)],
@@ -361,9 +361,10 @@ def alloc_strided_encoding(d: dict, device="cuda") -> Encoding:
     return alloc_cscc_encoding(d, device, caps=spc_strided_capacity(d))
 
 
-def cpo_encode_strided(d: dict, x: torch.Tensor, enc: Encoding, stream=None):
-    _check(_lib.cpo_encode_strided(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c), _stream(stream)),
-           "cpo_encode_strided")
+def cpo_encode_strided(d: dict, x: torch.Tensor, enc: Encoding, ws: torch.Tensor | None = None, stream=None):
+    _check(_lib.cpo_encode_strided(ctypes.byref(make_desc(d)), _ptr(x), ctypes.byref(enc.c),
+                                   _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
+                                   _stream(stream)), "cpo_encode_strided")
 
 
 def alloc_fused_workspace(d: dict, device="cuda") -> torch.Tensor:

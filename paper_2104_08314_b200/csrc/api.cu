@@ -447,16 +447,25 @@ spc_status spc_strided_capacity(const spc_conv_desc* d, int64_t* ptr_cap, int64_
     return SPC_OK;
 }
 
-spc_status cpo_encode_strided(const spc_conv_desc* d, const float* x, spc_encoding* out, void* stream) {
+spc_status cpo_encode_strided(const spc_conv_desc* d, const float* x, spc_encoding* out, void* ws, size_t ws_bytes,
+                              void* stream) {
     spc_status s = spc_strided_capacity(d, nullptr, nullptr, nullptr);
     if (s != SPC_OK) return s;
     if (!x || !out || !out->ptr || !out->da || !out->in || !out->chan_ptr_off || !out->chan_nz_off ||
         !out->chan_in_off || !out->lengths)
         return fail(SPC_EINVAL, "null pointer");
     if (out->ptr_cap < 0 || out->da_cap < 0 || out->in_cap < 0) return fail(SPC_EINVAL, "negative capacity");
+    const spc::Geom g = spc::make_geom(*d);
+    // single pass (the canonical encoder's kernel with the layout's column order and blocks) when
+    // a workspace is given and the canonical preconditions hold; else the three-launch encoder
+    static const bool three = [] { const char* e = getenv("SPC_SA_3PASS"); return e && atoi(e); }();
+    const bool one = ws && !three && check_sparse_geometry(d) == SPC_OK && aligned16(x) &&
+                     (size_t)spc::ws_layout(g).cps_in <= ws_bytes;
+    g_err.clear();
     out->algo = SPC_ALGO_CPO_SA;
     out->geom = *d;
-    return cuda_status(spc::launch_sa_encode(spc::make_geom(*d), x, out, (cudaStream_t)stream), "cpo_encode_strided");
+    if (one) return cuda_status(spc::launch_encode(g, false, x, out, ws, (cudaStream_t)stream, true), "cpo_encode_strided");
+    return cuda_status(spc::launch_sa_encode(g, x, out, (cudaStream_t)stream), "cpo_encode_strided");
 }
 
 // ------------------------------------------------------------ SI space bounds (NEXT-3)

@@ -247,7 +247,8 @@ __device__ __forceinline__ T warp_exclusive_scan(T v, T* total) {
 
 // Internal launchers (defined in the .cu files, called from api.cu).
 namespace spc {
-cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding* e, void* ws, cudaStream_t st);
+cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding* e, void* ws, cudaStream_t st,
+                          bool sa = false);
 cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaStream_t st);
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st);
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,

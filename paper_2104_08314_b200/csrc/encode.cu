@@ -95,9 +95,10 @@ __device__ __forceinline__ bool is_middle(const Geom& g, int w) {
 
 // shared-memory carve-up of one tile (host and device agree through this)
 struct EncSmem {
-    size_t planes, umask, msk, cnt, incnt, dab, inb, tab, pinfo, poff, total;
+    size_t planes, umask, msk, cnt, incnt, dab, inb, tab, pinfo, poff, sa_ord, sa_col, sa_last, total;
 };
-__host__ __device__ inline EncSmem enc_smem_layout(const Geom& g, int P) {
+__host__ __device__ inline int sa_ntypes_of(const Geom& g) { return (g.S + g.sw - 1) / g.sw; }
+__host__ __device__ inline EncSmem enc_smem_layout(const Geom& g, int P, bool sa = false) {
     EncSmem L;
     const size_t HW = (size_t)g.H * g.W, cols = (size_t)P * g.Wp;
     const size_t nrb = (g.H + 31) / 32;
@@ -111,8 +112,49 @@ __host__ __device__ inline EncSmem enc_smem_layout(const Geom& g, int P) {
     L.tab = align_up(L.inb + cols * sizeof(int), 16);              // [P][Wp] int4 column table
     L.pinfo = align_up(L.tab + cols * sizeof(int4), 16);           // [P][4]: plen, nnz, in_len, lower
     L.poff = align_up(L.pinfo + (size_t)P * 4 * sizeof(int), 16);   // [P][4] int64: ptr, da, in offsets, fits
-    L.total = align_up(L.poff + (size_t)P * 4 * sizeof(long long), 16);
+    L.sa_ord = align_up(L.poff + (size_t)P * 4 * sizeof(long long), 16);   // stride-aware: [Wp] stream order
+    L.sa_col = L.sa_ord + (sa ? (size_t)g.Wp * sizeof(int) : 0);            // [Wp] coverage | local column << 8
+    L.sa_last = L.sa_col + (sa ? (size_t)g.Wp * sizeof(int) : 0);           // [types][O_w] last owned column
+    L.total = align_up(L.sa_last + (sa ? (size_t)sa_ntypes_of(g) * g.Ow * sizeof(int) : 0), 16);
     return L;
+}
+
+// ---- stride-aware layout (reading A32, SI Eq. 2): partition s covers padded columns
+// [s*s_w, s*s_w + K_w); coverage, owner (first covering partition), local column, type = cov - 1
+__device__ __forceinline__ int sa_cov_e(const Geom& g, int w) {
+    const int hi = min(g.Ow - 1, w / g.sw);
+    const int lo = (w - g.S + 1 <= 0) ? 0 : (w - g.S + 1 + g.sw - 1) / g.sw;
+    return max(0, hi - lo + 1);
+}
+__device__ __forceinline__ int sa_owner_e(const Geom& g, int w) {
+    return (w - g.S + 1 <= 0) ? 0 : (w - g.S + 1 + g.sw - 1) / g.sw;
+}
+// ptr length of a stride-aware plane: per coverage type present in the geometry (ascending),
+// a block [t+1, c_0 .. c_{O_w-1}] or [t+1, NPF]; NPC = one entry.  Columns w = l0, l0 + nl, ...
+// of this thread; nl = 32: the warp's lanes split the columns (lane 0 gets the result)
+__device__ __forceinline__ void sa_plane_lengths(const Geom& g, const int* wc, int td, unsigned types,
+                                                 const int* sacol, int l0, int nl, int* pi) {
+    int tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int w = l0; w < g.Wp; w += nl) {
+        const int cv = sacol[w] & 0xFF;
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if (t == cv - 1) tot[t] += wc[w];
+    }
+    if (nl == 32) {
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if ((types >> t) & 1u) tot[t] = warp_sum(tot[t]);
+        if (l0 != 0) return;
+    }
+    int plen = 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        if ((types >> t) & 1u) plen += tot[t] ? (1 + g.Ow) : 2;
+    pi[0] = td ? plen : 1;
+    pi[1] = td;
+    pi[2] = td;
+    pi[3] = 0;
 }
 
 // ptr length (NPC | S=1 block | NOP + overlap blocks with NPF, SI Eq. 3), and the DA
@@ -136,7 +178,7 @@ __device__ __forceinline__ void plane_lengths(const Geom& g, const int* wc, int 
     pi[0] = plen; pi[1] = td; pi[2] = ti; pi[3] = lower;
 }
 
-template <bool CPS>
+template <bool CPS, bool SA>
 __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
     const Geom& g = a.g;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -162,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
     }
     __syncthreads();
 
-    const EncSmem L = enc_smem_layout(g, a.P);
+    const EncSmem L = enc_smem_layout(g, a.P, SA);
     float* planes = reinterpret_cast<float*>(smem_raw + L.planes);
     unsigned* msk = reinterpret_cast<unsigned*>(smem_raw + L.msk);   // [P][Wp][NW]
     int* cnt = reinterpret_cast<int*>(smem_raw + L.cnt);             // [P][Wp]
@@ -174,6 +216,42 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
     const int NRB = (g.H + 31) / 32;
     int* pinfo = reinterpret_cast<int*>(smem_raw + L.pinfo);
     long long* poff = reinterpret_cast<long long*>(smem_raw + L.poff);
+    int* sa_ord = reinterpret_cast<int*>(smem_raw + L.sa_ord);     // SA: padded column at stream position q
+    int* sa_last = reinterpret_cast<int*>(smem_raw + L.sa_last);   // SA: [type][partition] last owned column
+    int* sa_col = reinterpret_cast<int*>(smem_raw + L.sa_col);     // SA: coverage | local column << 8
+    __shared__ unsigned s_types;                                   // SA: coverage types present (bit t = type t)
+    if constexpr (SA) {
+        // the layout's column order (types ascending, columns ascending inside a type; columns no
+        // partition covers last -- they hold no stored NZE) and each partition's last owned column
+        // of every type: geometry only, once per CTA
+        if (threadIdx.x == 0) s_types = 0u;
+        for (int w = threadIdx.x; w < Wp; w += kThreads) {
+            const int cv = sa_cov_e(g, w);
+            sa_col[w] = cv | ((w - sa_owner_e(g, w) * g.sw) << 8);
+        }
+        __syncthreads();
+        for (int w = threadIdx.x; w < Wp; w += kThreads) {
+            const int cv = sa_col[w] & 0xFF, key = cv ? cv : 1 << 20;
+            int q = 0;
+            for (int w2 = 0; w2 < Wp; w2++) {
+                const int c2 = sa_col[w2] & 0xFF, k2 = c2 ? c2 : 1 << 20;
+                q += (k2 < key) || (k2 == key && w2 < w);
+            }
+            sa_ord[q] = w;
+            if (cv) atomicOr(&s_types, 1u << (cv - 1));
+        }
+        const int nt = sa_ntypes_of(g);
+        for (int i = threadIdx.x; i < nt * g.Ow; i += kThreads) {
+            const int t = i / g.Ow, s2 = i % g.Ow;
+            int last = -1;
+            for (int l = 0; l < g.S; l++) {
+                const int w = s2 * g.sw + l;
+                if (w < Wp && (sa_col[w] & 0xFF) == t + 1 && (sa_col[w] >> 8) == l) last = w;
+            }
+            sa_last[i] = last;
+        }
+        __syncthreads();
+    }
 
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
         const long long plane0 = (long long)tile * a.P;
@@ -253,13 +331,14 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
             const unsigned* u = umask + ((size_t)p * g.W + (real ? col : 0)) * NRB;
             int c = 0, e = 0;
             const bool mid = CPS && is_middle(g, w);
+            const bool stored = !SA || (sa_col[w] & 0xFF) > 0;   // SA: columns no partition covers are not stored
             unsigned prev = 0;
             for (int j = 0; j < NW; j++) {
                 const unsigned uj = (real && j < NRB) ? u[j] : 0u;
                 const unsigned m = g.pt ? ((uj << g.pt) | (prev >> (32 - g.pt))) : uj;
                 prev = uj;
                 msk[it * NW + j] = m;
-                c += __popc(m);
+                c += stored ? __popc(m) : 0;
                 if (mid) {
 #pragma unroll
                     for (int q = 0; q < 8; q++) {
@@ -282,13 +361,14 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
                 const int* wi = incnt + p * Wp;
                 int ed = 0, ei = 0;
                 for (int q = 0; q < Wp; q++) {
-                    const int w = col_at(g, q);
+                    const int w = SA ? sa_ord[q] : col_at(g, q);
                     dab[p * Wp + w] = ed;
                     inb[p * Wp + w] = ei;
                     ed += wc[w];
                     ei += wi[w];
                 }
-                plane_lengths(g, wc, ed, ei, pinfo + 4 * p);
+                if (SA) sa_plane_lengths(g, wc, ed, s_types, sa_col, 0, 1, pinfo + 4 * p);
+                else plane_lengths(g, wc, ed, ei, pinfo + 4 * p);
             }
         } else {
             for (int p = warp; p < np; p += kEncWarps) {
@@ -298,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
                 const int q0 = lane * per, q1 = min(q0 + per, Wp);
                 int sd = 0, si = 0;
                 for (int q = q0; q < q1; q++) {
-                    const int w = col_at(g, q);
+                    const int w = SA ? sa_ord[q] : col_at(g, q);
                     sd += wc[w];
                     si += wi[w];
                 }
@@ -306,13 +386,14 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
                 int ed = warp_exclusive_scan(sd, &td);
                 int ei = warp_exclusive_scan(si, &ti);
                 for (int q = q0; q < q1; q++) {
-                    const int w = col_at(g, q);
+                    const int w = SA ? sa_ord[q] : col_at(g, q);
                     dab[p * Wp + w] = ed;
                     inb[p * Wp + w] = ei;
                     ed += wc[w];
                     ei += wi[w];
                 }
-                if (lane == 0) plane_lengths(g, wc, td, ti, pinfo + 4 * p);
+                if (SA) sa_plane_lengths(g, wc, td, s_types, sa_col, lane, 32, pinfo + 4 * p);
+                else if (lane == 0) plane_lengths(g, wc, td, ti, pinfo + 4 * p);
             }
         }
         __syncthreads();
@@ -422,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
             const bool wr_in = !(CPS && is_middle(g, w));
             tab[it] = make_int4((int)(poff[4 * p + 1] - Z0) + dab[it], (int)(poff[4 * p + 2] - Q0) + inb[it],
                                 p * HW + (w - g.pl) - g.pt * g.W,
-                                local_of(g, w) | (wr_in ? kTabIn : 0) | (ok ? kTabOk : 0));
+                                (SA ? sa_col[w] >> 8 : local_of(g, w)) | (wr_in ? kTabIn : 0) |
+                                    (ok ? kTabOk : 0));
         }
         __syncthreads();
 
@@ -435,6 +517,30 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
             int32_t* pp = a.ptr + poff[4 * p];
             if (nnz == 0) {
                 if (lane == 0) pp[0] = SPC_NPC;
+            } else if (SA) {
+                // stride-aware blocks (reading A32): per type present, [t+1, c_0 .. c_{O_w-1}] with
+                // c_s = block-relative cumulative count through partition s's last owned type-t
+                // column (-1: owns none), or [t+1, NPF]
+                const int* wd = dab + p * Wp;
+                int pos = 0, run = 0;
+                for (int t = 0; t < sa_ntypes_of(g); t++) {
+                    if (!((s_types >> t) & 1u)) continue;
+                    long long tl = 0;
+                    for (int w = lane; w < Wp; w += 32) tl += ((sa_col[w] & 0xFF) == t + 1) ? wc[w] : 0;
+                    const int tt = (int)warp_sum(tl);
+                    if (lane == 0) pp[pos] = t + 1;
+                    if (tt == 0) {
+                        if (lane == 0) pp[pos + 1] = SPC_NPF;
+                        pos += 2;
+                        continue;
+                    }
+                    for (int s2 = lane; s2 < g.Ow; s2 += 32) {
+                        const int last = sa_last[t * g.Ow + s2];
+                        pp[pos + 1 + s2] = (last < 0) ? -1 : wd[last] + wc[last] - run;
+                    }
+                    run += tt;
+                    pos += 1 + g.Ow;
+                }
             } else if (g.S == 1) {
                 if (lane == 0) pp[0] = 0;
                 const int* wd = dab + p * Wp;
@@ -644,7 +750,7 @@ int sm_count() { return device_sm_count(); }
 // that many rounds, so every round is (nearly) full.  Measured: cfg5-L7 (batch 32) 71 -> 50 us
 // (a 51-plane tile at 1 CTA/SM had left a 13-tile second round), batch 256 L4 176 -> 147 us,
 // L14 137 -> 102 us; one-round launches are unchanged (cfg2: P = 1, cfg5-L0: P = 7).
-EncPlan plan_encode(const Geom& g) {
+EncPlan plan_encode(const Geom& g, bool sa = false) {
     EncPlan pl;
     const int sms = sm_count();
     const size_t b2 = 110 * 1024, b1 = 220 * 1024;
@@ -652,17 +758,17 @@ EncPlan plan_encode(const Geom& g) {
     for (int per_sm = 2; per_sm >= 1 && P == 0; per_sm--) {
         const size_t budget = (per_sm == 2) ? b2 : b1;
         long long pmax = 0;
-        while (pmax < g.NC && enc_smem_layout(g, (int)(pmax + 1)).total <= budget) pmax++;
+        while (pmax < g.NC && enc_smem_layout(g, (int)(pmax + 1), sa).total <= budget) pmax++;
         if (pmax == 0) continue;
         const long long slots = (long long)per_sm * sms;
         const long long rounds = (g.NC + slots * pmax - 1) / (slots * pmax);
         P = (g.NC + slots * rounds - 1) / (slots * rounds);
     }
     static const int force_p = [] { const char* v = getenv("SPC_ENC_P"); return v ? atoi(v) : 0; }();
-    if (force_p > 0 && enc_smem_layout(g, force_p).total <= b1) P = force_p;   // development A/B
+    if (force_p > 0 && enc_smem_layout(g, force_p, sa).total <= b1) P = force_p;   // development A/B
     pl.P = (int)std::max(1ll, P);
     pl.ntiles = (int)((g.NC + pl.P - 1) / pl.P);
-    pl.smem = enc_smem_layout(g, pl.P).total;
+    pl.smem = enc_smem_layout(g, pl.P, sa).total;
     pl.grid = pl.ntiles;
     return pl;
 }
@@ -671,7 +777,8 @@ EncPlan plan_encode(const Geom& g) {
 
 size_t enc_smem_bytes(const Geom& g) { return plan_encode(g).smem; }
 
-cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding* e, void* ws, cudaStream_t st) {
+cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding* e, void* ws, cudaStream_t st,
+                          bool sa) {
     WsLayout W = ws_layout(g);
     EncArgs a;
     a.g = g; a.x = x;
@@ -682,13 +789,13 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
     unsigned char* base = static_cast<unsigned char*>(ws);
     a.st = reinterpret_cast<EncState*>(base + W.state);
     a.agg = reinterpret_cast<unsigned long long*>(base + W.agg);
-    EncPlan pl = plan_encode(g);
+    EncPlan pl = plan_encode(g, sa);
     a.P = pl.P;
     a.ntiles = pl.ntiles;
-    void (*kern)(EncArgs) = cps ? encode_kernel<true> : encode_kernel<false>;
-    static std::atomic<size_t> attr_bytes[2][kMaxDevices];
+    void (*kern)(EncArgs) = sa ? encode_kernel<false, true> : cps ? encode_kernel<true, false> : encode_kernel<false, false>;
+    static std::atomic<size_t> attr_bytes[3][kMaxDevices];
     {
-        cudaError_t err = ensure_smem_attr((const void*)kern, pl.smem, attr_bytes[cps]);
+        cudaError_t err = ensure_smem_attr((const void*)kern, pl.smem, attr_bytes[sa ? 2 : cps ? 1 : 0]);
         if (err != cudaSuccess) return err;
     }
     // the cross-tile prefix needs every CTA resident: cap the grid at the

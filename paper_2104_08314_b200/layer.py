@@ -67,7 +67,7 @@ class SparseConvLayer:
             return self.y
         if algo == "cpo_sa":         # stride-aware CPO layout (reading A32)
             e = self.extra_encoding(algo)
-            B.cpo_encode_strided(self.d, x, e)
+            B.cpo_encode_strided(self.d, x, e, self.ws)
             B.sparse_conv_forward(self.d, e, self.wp, self.y, self.relu, self.ws)
             return self.y
         if algo == "im2col" or not self.sparse_ok:

@@ -14,7 +14,8 @@ for name in sys.argv[1:]:
         a.record()
         for _ in range(n): fn()
         b.record(); torch.cuda.synchronize(); return a.elapsed_time(b) / n * 1e3
-    te = t(lambda: spc.cpo_encode_strided(d, x, e))
+    te = t(lambda: spc.cpo_encode_strided(d, x, e, L.ws))
+    te3 = t(lambda: spc.cpo_encode_strided(d, x, e))
     tc = t(lambda: spc.sparse_conv_forward(d, e, L.wp, L.y, False, L.ws))
     te0 = t(lambda: L.encode(x)); tc0 = t(lambda: L.conv())
-    print(name, "sa enc %.1f conv %.1f | cpo enc %.1f conv %.1f" % (te, tc, te0, tc0))
+    print(name, "sa enc %.1f (3 launches %.1f) conv %.1f | cpo enc %.1f conv %.1f" % (te, te3, tc, te0, tc0))
