@@ -540,12 +540,18 @@ static bool plan_ws(const Geom& g, int pmax, WsPlan<T>& p) {
 template <class T>
 static cudaError_t run_ws(ConvArgs& a, cudaStream_t st) {
     const Geom& g = a.g;
-    // stride-aware encodings run on the strip kernel (its per-channel P1 takes the (partition, type)
-    // slots; the producers' path here faulted on the 28 -> 14 layer and is not used)
-    if (a.sa_types || a.cscc) return cudaErrorNotSupported;
+    // CSCC encodings run on the strip kernel (its P1 reads CSCC's per-submatrix rows); the
+    // stride-aware layout's (partition, type) slots are parsed by the producers here as well
+    // (SPC_WS_SLOTS=0: strip kernel, development A/B)
+    static const int ws_slots = [] { const char* v = getenv("SPC_WS_SLOTS"); return v ? atoi(v) : 1; }();
+    if (a.cscc || (a.sa_types && !ws_slots)) return cudaErrorNotSupported;
     WsPlan<T> p;
     if (!plan_ws<T>(g, a.pmax, p)) return cudaErrorNotSupported;
-    if (p.cg > 1 && (!a.scratch || a.scratch_bytes < p.scratch_bytes)) p.cg = 1;   // no scratch: no split
+    if (p.cg > 1 && (!a.scratch || a.scratch_bytes < p.scratch_bytes)) {          // no scratch: no split
+        p.cg = 1;
+        p.smem = ws_smem_layout<T>(p.RT, a.pmax, g.C).total;   // one CTA's side tables cover every channel
+        if (p.smem > 227 * 1024) return cudaErrorNotSupported;
+    }
     WsArgs wa;
     wa.a = a;
     wa.a.cg = p.cg;

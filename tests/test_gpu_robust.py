@@ -119,3 +119,32 @@ def test_conv_over_flagged_encoding_writes_zeros():
     L2.enc.lengths.fill_(1)
     L2.encode(torch.from_numpy(x).cuda())
     assert L2.conv().abs().sum().item() > 0
+
+
+@pytest.mark.parametrize("shape", [(1, 256, 14, 14, 256, 1), (1, 128, 28, 28, 256, 2), (1, 512, 7, 7, 512, 1)])
+def test_conv_without_workspace_on_cluster_shapes(oracle_mod, shape):
+    """Warp-specialised conv shapes whose plan splits the input channels over a cluster when a
+    workspace (L2 partials) is given: without one the launch falls back to one CTA per unit and
+    must size its shared memory for all the channels (round 2 regression: the side tables were
+    sized for the split, the barriers landed outside the allocation).  CPO and the stride-aware
+    layout, integer data, exact."""
+    N, C, H, W, K, st = shape
+    d = layer_desc(N, C, H, W, K, 3, 3, st, st, 1, 1, 1, 1)
+    x = int_map(N, C, H, W, 0.2, 17)
+    w = int_weights(K, C, 3, 3, 17)
+    ref = oracle_mod.direct_conv(d, x, w).astype(np.float32)
+    xg, wg = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    wp = torch.empty_like(wg).reshape(-1)
+    spc.spc_pack_weights(d, wg, wp)
+    Oh, Ow = spc.spc_output_dims(d)
+    ws = spc.alloc_workspace(d)
+    for strided in (False, True):
+        enc = spc.alloc_strided_encoding(d) if strided else spc.alloc_encoding(d)
+        if strided:
+            spc.cpo_encode_strided(d, xg, enc, ws)
+        else:
+            spc.cpo_encode(d, xg, enc, ws)
+        for conv_ws in (None, ws):
+            y = torch.full((N, K, Oh, Ow), float("nan"), device="cuda")
+            spc.sparse_conv_forward(d, enc, wp, y, False, conv_ws)
+            assert np.array_equal(y.cpu().numpy(), ref), (strided, conv_ws is None)
