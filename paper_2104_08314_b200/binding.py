@@ -8,6 +8,7 @@ module raises if the compiled sm_100a library is missing.
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 from dataclasses import dataclass, field
 
@@ -379,3 +380,31 @@ def sparse_conv_encode_forward(d: dict, enc: Encoding, w_packed: torch.Tensor, y
     _check(_lib.sparse_conv_encode_forward(ctypes.byref(make_desc(d)), ctypes.byref(enc.c), _ptr(w_packed), _ptr(y),
                                            int(fuse_relu), ctypes.byref(make_desc(next_d)), ctypes.byref(out.c),
                                            _ptr(ws), ws.numel(), _stream(stream)), "sparse_conv_encode_forward")
+
+
+# ---- device routing: the C ABI launches on the CURRENT device, so every wrapper that
+# passes tensors runs with the device of its first CUDA tensor (or encoding) made current.
+def _device_of(args, kwargs):
+    for a in (*args, *kwargs.values()):
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            return a.device
+        if isinstance(a, Encoding) and a.ptr.is_cuda:
+            return a.ptr.device
+    return None
+
+
+def _on_device(fn):
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        dev = _device_of(args, kwargs)
+        if dev is None or dev.index is None or dev.index == torch.cuda.current_device():
+            return fn(*args, **kwargs)
+        with torch.cuda.device(dev):
+            return fn(*args, **kwargs)
+    return wrapped
+
+
+for _name in ("spc_workspace_init", "cpo_encode", "cps_encode", "spc_pack_weights", "sparse_conv_forward",
+              "im2col_conv_forward", "select_layer_algo", "spc_validate_encoding", "spc_encoding_lengths",
+              "cscc_encode", "cscc_conv_forward", "cpo_encode_strided", "sparse_conv_encode_forward"):
+    globals()[_name] = _on_device(globals()[_name])
