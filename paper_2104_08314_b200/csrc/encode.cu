@@ -355,7 +355,14 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(EncArgs a) {
         // ---- 4. per plane: stream-order exclusive prefix over columns, plane totals and
         //         the ptr length (SI Eq. 3 with the actual NPF count); thread per plane for
         //         narrow planes, warp per plane otherwise
+        // (thread per plane only when the tile has more planes than warps: a few planes of a
+        //  narrow map are scanned faster by a warp each -- cfg3: 7 planes of Wp = 16)
+        static_assert(kEncWarps >= 8, "");
+#ifndef SPC_ENC_THREAD_SCAN
+        if (Wp <= 24 && np > kEncWarps) {
+#else
         if (Wp <= 24) {
+#endif
             for (int p = threadIdx.x; p < np; p += kThreads) {
                 const int* wc = cnt + p * Wp;
                 const int* wi = incnt + p * Wp;
