@@ -238,6 +238,11 @@ spc_gemm spc_get_im2col_gemm(void);
  * SPC_GEMM_AUTO and the tcgen05 engine's C*R*S % 4 fallback); host only. */
 spc_gemm spc_im2col_engine(const spc_conv_desc *d);
 
+/* Which kernel the calling host thread's last sparse_conv_forward / sparse_conv_encode_forward
+ * (CPO, CPS or stride-aware encoding) launched: 2 = warp-specialised (ws_conv_kernel), 1 = strip
+ * (strip_conv_kernel), 0 = generic, -1 = none yet.  Host only (benchmarks, tests). */
+int spc_last_conv_kernel(void);
+
 /* Host, synchronising (it times).  Per-layer offline selection:
  * over the M sample maps (device, M*N*C*H*W fp32), time encode+conv for CPO
  * and CPS and lowering+GEMM for im2col, `reps` times each, sum per algorithm

@@ -89,6 +89,8 @@ _lib.spc_set_im2col_gemm.restype = ctypes.c_int
 _lib.spc_get_im2col_gemm.argtypes = []
 _lib.spc_get_im2col_gemm.restype = ctypes.c_int
 _lib.spc_im2col_engine.argtypes = [ctypes.c_void_p]
+_lib.spc_last_conv_kernel.argtypes = []
+_lib.spc_last_conv_kernel.restype = ctypes.c_int
 _lib.spc_im2col_engine.restype = ctypes.c_int
 _lib.spc_im2col_ws_bytes.argtypes = [ctypes.c_void_p]
 _lib.spc_im2col_ws_bytes.restype = ctypes.c_size_t
@@ -100,7 +102,7 @@ _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
 EXPORTED = list(_sigs) + ["spc_fused_ws_bytes", "spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
-                          "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes"]
+                          "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes", "spc_last_conv_kernel"]
 SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
 SPC_GEMM_AUTO = 5
 GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
@@ -129,6 +131,15 @@ def spc_im2col_ws_bytes(d: dict) -> int:
 def alloc_im2col_workspace(d: dict, device="cuda") -> torch.Tensor:
     """fp32 workspace of spc_im2col_ws_bytes(d) bytes (lowered matrix + split weights)."""
     return torch.empty((spc_im2col_ws_bytes(d) + 3) // 4, dtype=torch.float32, device=device)
+
+
+CONV_KERNELS = {2: "ws_conv_kernel (warp-specialised)", 1: "strip_conv_kernel", 0: "sparse_conv_generic_kernel",
+                -1: "none"}
+
+
+def spc_last_conv_kernel() -> int:
+    """Kernel of this thread's last sparse conv launch (CONV_KERNELS)."""
+    return int(_lib.spc_last_conv_kernel())
 
 
 def spc_im2col_engine(d: dict) -> int:

@@ -311,6 +311,8 @@ spc_status spc_set_im2col_gemm(spc_gemm gemm) {
 
 spc_gemm spc_get_im2col_gemm(void) { return (spc_gemm)spc::gemm_engine(); }
 
+int spc_last_conv_kernel(void) { return spc::last_conv_kernel(); }
+
 size_t spc_im2col_ws_bytes(const spc_conv_desc* d) {
     if (!d || check_desc(d) != SPC_OK) return 0;
     const spc::Geom g = spc::make_geom(*d);

@@ -251,6 +251,7 @@ cudaError_t launch_encode(const Geom& g, bool cps, const float* x, spc_encoding*
                           bool sa = false);
 cudaError_t launch_pack_weights(const Geom& g, const float* w, float* wp, cudaStream_t st);
 cudaError_t launch_cps_expand(const Geom& g, const spc_encoding* e, int32_t* in_cpo, cudaStream_t st);
+int last_conv_kernel();   // sparse_conv.cu: kernel of this thread's last sparse-conv launch
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
                                cudaStream_t st, unsigned long long* omask = nullptr, unsigned sa_types = 0,

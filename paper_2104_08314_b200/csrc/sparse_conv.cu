@@ -1612,6 +1612,11 @@ size_t conv_scratch_bytes(const Geom& g) {
     return bytes ? kSkFlagBytes + bytes : 0;
 }
 
+// which kernel the calling thread's last sparse-conv launch ran (2 warp-specialised, 1 strip,
+// 0 generic, -1 none yet): reported by spc_last_conv_kernel() for benchmarks and tests
+static thread_local int t_last_conv_kernel = -1;
+int last_conv_kernel() { return t_last_conv_kernel; }
+
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
                                cudaStream_t st, unsigned long long* omask, unsigned sa_types, int cscc) {
@@ -1649,9 +1654,15 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     if (sa_types || cscc) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
     cudaError_t err = cudaErrorNotSupported;
     if (!conv_v1_forced()) err = visit_ws_cfg(g, [&](auto cfg) { return run_ws<decltype(cfg)>(a, st); });
-    if (err != cudaErrorNotSupported) return err;
+    if (err != cudaErrorNotSupported) {
+        t_last_conv_kernel = 2;
+        return err;
+    }
     err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
-    if (err != cudaErrorNotSupported) return err;
+    if (err != cudaErrorNotSupported) {
+        t_last_conv_kernel = 1;
+        return err;
+    }
     if (sa_types || cscc) return cudaErrorNotSupported;   // the layout's own kernel runs instead
     // generic
     const int WH = (kGenTY - 1) * g.sh + g.R, WW = (kGenTX - 1) * g.sw + g.S;
@@ -1672,6 +1683,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    t_last_conv_kernel = 0;
     return cudaLaunchKernelEx(&cfg, sparse_conv_generic_kernel, a, WH, WW);
 }
 

@@ -148,3 +148,16 @@ def test_conv_without_workspace_on_cluster_shapes(oracle_mod, shape):
             y = torch.full((N, K, Oh, Ow), float("nan"), device="cuda")
             spc.sparse_conv_forward(d, enc, wp, y, False, conv_ws)
             assert np.array_equal(y.cpu().numpy(), ref), (strided, conv_ws is None)
+
+
+def test_last_conv_kernel_reports_the_launch():
+    """spc_last_conv_kernel names the kernel the last sparse conv launched (bench's roofline label):
+    the warp-specialised kernel on cfg3's 14x14 @ 256 layer, the strip kernel on cfg2's 56x56 @ 64."""
+    for name, kind in (("cfg3", 2), ("cfg2", 1)):
+        d = CONFIGS[name]["desc"]
+        x = clustered_relu(d["N"], d["C"], d["H"], d["W"], 0.1, 3)
+        L = GpuLayer(d, he_normal(d["K"], d["C"], 3, 3, 3))
+        L.encode(torch.from_numpy(x).cuda())
+        L.conv()
+        torch.cuda.synchronize()
+        assert spc.spc_last_conv_kernel() == kind, (name, spc.spc_last_conv_kernel())
