@@ -446,14 +446,34 @@ __global__ void __launch_bounds__(256) cps_expand_warp_kernel(Geom g, const int3
     pdl_trigger();
     if (nc >= g.NC) return;
     if (*reinterpret_cast<volatile const unsigned long long*>(status) != 0ull) return;   // flagged encoding
-    const long long Z = cnz_off[nc], Q = cin_off[nc];
-    const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q);
+    const long long Z = cnz_off[nc], Q = cin_off[nc], P = cpo_off[nc];
+    const int nnz = (int)(cnz_off[nc + 1] - Z), nin = (int)(cin_off[nc + 1] - Q), plen = (int)(cpo_off[nc + 1] - P);
     if (nnz == 0) return;
     const int e0 = (lane < nin) ? __ldg(in + Q + lane) : 0;   // in flight during the directory parse
     int dmid = nnz;
-    if (g.S > 1) {
+    if (g.S > 1 && plen <= 64) {
+        // the channel's ptr segment in two registers per lane (one round trip), the block
+        // directory walked by shuffles: DA start of the overlapK_w block (Alg. 1 layout)
+        const int v0 = (lane < plen) ? __ldg(ptr + P + lane) : 0;
+        const int v1 = (32 + lane < plen) ? __ldg(ptr + P + 32 + lane) : 0;
+        auto seg = [&](int i) {
+            const int a0 = __shfl_sync(0xffffffffu, v0, i & 31), a1 = __shfl_sync(0xffffffffu, v1, i & 31);
+            return i < 32 ? a0 : a1;
+        };
+        int p = 0, dacur = 0;
+        if (g.pl == 0) {                             // NOP [0, a, a+b]
+            dacur = seg(2);
+            p = 3;
+        }
+        for (int t = max(1, g.pl); t <= g.S - 2; t++) {
+            if (seg(p + 1) == SPC_NPF) { p += 2; continue; }
+            dacur += seg(p + 1 + (g.Ow1 - 1 - t));
+            p += 1 + g.Ow1;
+        }
+        dmid = (seg(p + 1) == SPC_NPF) ? nnz : dacur;
+    } else if (g.S > 1) {
         ChanDir d;
-        parse_channel(g, ptr, cpo_off[nc], d);
+        parse_channel(g, ptr, P, d);
         dmid = (d.pos[g.S - 1] >= 0) ? d.da[g.S - 1] : nnz;
     }
     if (lane < dmid) out[Z + lane] = e0;
