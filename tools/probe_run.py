@@ -49,11 +49,11 @@ for wl in sys.argv[1:] or ["cfg1", "cfg2"]:
     xg, wg = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
     L = SparseConvLayer(d, wg)
     for _ in range(3):
-        L.forward(xg, "cpo")
+        L.forward(xg, os.environ.get("PROBE_ALGO", "cpo"))
     torch.cuda.synchronize()
     grab(lib.spc_debug_probes_enc); grab(lib.spc_debug_probes_conv)
     if os.environ.get("PROBE_GRAPH"):
-        gr = L.capture(lambda: L.forward(xg, "cpo"))
+        gr = L.capture(lambda: L.forward(xg, os.environ.get("PROBE_ALGO", "cpo")))
         gr.replay()
         torch.cuda.synchronize()
         grab(lib.spc_debug_probes_enc); grab(lib.spc_debug_probes_conv)
@@ -62,7 +62,7 @@ for wl in sys.argv[1:] or ["cfg1", "cfg2"]:
     if os.environ.get("PROBE_GRAPH"):
         gr.replay()
     else:
-        L.forward(xg, "cpo")
+        L.forward(xg, os.environ.get("PROBE_ALGO", "cpo"))
     torch.cuda.synchronize()
     e, cv = grab(lib.spc_debug_probes_enc), grab(lib.spc_debug_probes_conv)
     print(f"== {wl}")
