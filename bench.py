@@ -244,7 +244,10 @@ def run_reference(args):
             "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"]},
+            # the same config object as the GPU arm's line (its L2 plan is host arithmetic)
+            "config": {"workload": args.workload, **{k: d[k] for k in d}, "density": c["density"],
+                       "dead_frac": c["dead_frac"], "zero_tile_frac": c["zero_tile_frac"],
+                       "l2": l2_note_of(*l2_plan(d, make_pool(c, 0))), "global_batch": d["N"] * max(1, args.gpus)},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
                              "sample": f"{imgs} image(s) of {args.workload} over {args.steps} steps"},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -266,16 +269,7 @@ class Rotating:
         from paper_2104_08314_b200.layer import SparseConvLayer
         self.d, self.dev = d, dev
         N = d["N"]
-        Oh, Ow = spc_out_hw(d)
-        rho = float((pool != 0).mean())
-        x_b = 4 * N * d["C"] * d["H"] * d["W"]
-        enc_b = 2 * 8 * rho * N * d["C"] * d["H"] * d["W"] + 4 * N * d["C"] * (3 + 2 * (d["W"] + 2))
-        w_b = 4 * d["K"] * d["C"] * d["R"] * d["S"]
-        y_b = 4 * N * d["K"] * Oh * Ow
-        self.touched = x_b + enc_b + w_b + y_b          # per step (encode reads x, writes enc; conv reads enc, w)
-        need = int(np.ceil(1.5 * L2_BYTES / self.touched))
-        self.cold = need <= max_sets
-        self.nset = max(min_sets, min(need, max_sets)) if self.cold else min_sets
+        self.nset, self.cold, self.touched = l2_plan(d, pool, min_sets, max_sets)
         self.layers, self.xs = [], []
         nd = pool.shape[0]
         for i in range(self.nset):
@@ -345,10 +339,31 @@ class Rotating:
         return ev0.elapsed_time(ev1)
 
     def l2_note(self) -> str:
-        if self.cold:
-            return (f"inputs larger than L2: back-to-back steps over {self.nset} buffer sets, "
-                    f"~{self.nset * self.touched / 2**20:.0f} MiB touched per cycle (L2 126 MiB)")
-        return f"L2 flushed between steps (2x-L2 write; {self.nset} sets would not exceed L2)"
+        return l2_note_of(self.nset, self.cold, self.touched)
+
+
+def l2_plan(d, pool, min_sets=4, max_sets=128):
+    """Rotating buffer sets for L2-cold steps: (sets, cold, bytes touched per step).  Host arithmetic
+    only (the reference arm states the same plan in its config)."""
+    N = d["N"]
+    Oh = (d["H"] + d["pad_top"] + d["pad_bottom"] - d["R"]) // d["stride_h"] + 1
+    Ow = (d["W"] + d["pad_left"] + d["pad_right"] - d["S"]) // d["stride_w"] + 1
+    rho = float((pool != 0).mean())
+    x_b = 4 * N * d["C"] * d["H"] * d["W"]
+    enc_b = 2 * 8 * rho * N * d["C"] * d["H"] * d["W"] + 4 * N * d["C"] * (3 + 2 * (d["W"] + 2))
+    w_b = 4 * d["K"] * d["C"] * d["R"] * d["S"]
+    y_b = 4 * N * d["K"] * Oh * Ow
+    touched = x_b + enc_b + w_b + y_b          # per step (encode reads x, writes enc; conv reads enc, w)
+    need = int(np.ceil(1.5 * L2_BYTES / touched))
+    cold = need <= max_sets
+    return (max(min_sets, min(need, max_sets)) if cold else min_sets), cold, touched
+
+
+def l2_note_of(nset, cold, touched) -> str:
+    if cold:
+        return (f"inputs larger than L2: back-to-back steps over {nset} buffer sets, "
+                f"~{nset * touched / 2**20:.0f} MiB touched per cycle (L2 126 MiB)")
+    return f"L2 flushed between steps (2x-L2 write; {nset} sets would not exceed L2)"
 
 
 def spc_out_hw(d):
