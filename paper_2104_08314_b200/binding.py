@@ -133,7 +133,7 @@ def alloc_im2col_workspace(d: dict, device="cuda") -> torch.Tensor:
     return torch.empty((spc_im2col_ws_bytes(d) + 3) // 4, dtype=torch.float32, device=device)
 
 
-CONV_KERNELS = {2: "ws_conv_kernel (warp-specialised)", 1: "strip_conv_kernel", 0: "sparse_conv_generic_kernel",
+CONV_KERNELS = {3: "tile_conv_kernel (register-tiled)", 2: "ws_conv_kernel (warp-specialised)", 1: "strip_conv_kernel", 0: "sparse_conv_generic_kernel",
                 -1: "none"}
 
 

@@ -1611,6 +1611,7 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
 }
 
 #include "ws_conv.cuh"
+#include "tile_conv.cuh"
 
 static bool conv_v1_forced() {   // development A/B: SPC_CONV_V1=1 runs the round-1 strip kernel
     static const char* env = getenv("SPC_CONV_V1");
@@ -1632,7 +1633,7 @@ size_t conv_scratch_bytes(const Geom& g) {
     return bytes ? kSkFlagBytes + bytes : 0;
 }
 
-// which kernel the calling thread's last sparse-conv launch ran (2 warp-specialised, 1 strip,
+// which kernel the calling thread's last sparse-conv launch ran (3 register-tiled, 2 warp-specialised, 1 strip,
 // 0 generic, -1 none yet): reported by spc_last_conv_kernel() for benchmarks and tests
 static thread_local int t_last_conv_kernel = -1;
 int last_conv_kernel() { return t_last_conv_kernel; }
@@ -1673,6 +1674,11 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
     if (sa_types || cscc) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
     cudaError_t err = cudaErrorNotSupported;
+    if (!conv_v1_forced()) err = visit_tc_cfg(g, [&](auto cfg) { return run_tc<decltype(cfg)>(a, st); });
+    if (err != cudaErrorNotSupported) {
+        t_last_conv_kernel = 3;
+        return err;
+    }
     if (!conv_v1_forced()) err = visit_ws_cfg(g, [&](auto cfg) { return run_ws<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) {
         t_last_conv_kernel = 2;
