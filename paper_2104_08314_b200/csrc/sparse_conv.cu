@@ -734,7 +734,7 @@ __device__ int sk_start(const ConvArgs& a, int b) {
 //      cost multiply-adds (Alg. 2 convSpMv), with no indirect branches.
 // Epilogue: reduce the csplit warps of a row tile through smem, then the cg
 // CTAs of the cluster through distributed shared memory; ReLU; NKHW store.
-template <class T, bool BAL>
+template <class T, bool BAL, bool SL = false>   // SL: stride-aware / CSCC slot parse (P1)
 __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
@@ -863,20 +863,24 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             probe(1);
             pdl_wait();
             probe(2);
-            // an encoding the encoder flagged (capacity overflow / wait timeout) is not read:
-            // the unit's output is written as zeros (all threads read the same word)
-            if (*reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull) {
-                bad = true;
-                cp_async_wait_all();   // the prologue's tap copies land before smem is reused
-            }
         }
+        // an encoding the encoder flagged (capacity overflow / wait timeout) is not read: the
+        // unit's output is written as zeros (all threads read the same word).  The word is loaded
+        // together with the side tables (in bounds whatever the flag), not ahead of them.
+        unsigned long long st0 = 0ull;
+        if (first) st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
         int buf = 0;
-        if (c_begin < c_end && !bad) {
-            stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
-            if (BAL && threadIdx.x == 0) s_seg[0] = t_next;
-            stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
+        if (c_begin < c_end) stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
+        if (st0 != 0ull && !bad) {
+            bad = true;
+            cp_async_wait_all();   // the prologue's tap copies land before smem is reused
         }
-        for (int c0 = c_begin; c0 < c_end && !bad; c0 += CHS, buf ^= 1) {
+        // the balanced mode's range advances whatever the flag (a flagged encoding's segments are
+        // walked as empty: zero partials, published and summed as usual)
+        if (BAL && threadIdx.x == 0 && c_begin < c_end) s_seg[0] = t_next;
+        if (c_begin < c_end && !bad) stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
+        const int c_stop = bad ? c_begin : c_end;
+        for (int c0 = c_begin; c0 < c_stop; c0 += CHS, buf ^= 1) {
             const int chn = min(CHS, c_end - c0);
             const bool stage = !(dev_phase_mode() == 1 && !(first && c0 == c_begin));
             // ---- P0: taps (cp.async, with this chunk's prefetched ptr segments in flight); zero the windows
@@ -892,7 +896,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             // type) pairs of the stride-aware layout, submatrices of CSCC -- whose NZE column is the
             // slot's base + IN % K_w (so the canonical path keeps its compile-time column bounds)
             auto run_p1 = [&](auto slots_c) {
-                constexpr bool SL = decltype(slots_c)::value;
             if constexpr (T::FLAT) {
                 // ---- P1: scatter every NZE of the strip's window columns into its row tiles' windows.
                 //      (a) warp per channel: block directory (NPC / NPF skip) and the DA range of each
@@ -1064,8 +1067,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 }
             }
             };
-            if (a.sa_types || a.cscc) run_p1(std::true_type{});
-            else run_p1(std::false_type{});
+            // (a compile-time choice: the canonical kernel does not carry the slot parse's registers)
+            run_p1(std::integral_constant<bool, SL>{});
             if (stage) __syncthreads();
             if (c0 == c_begin) probe(4);
             // prefetch the next chunk's ptr segments (its buffer was last read before the barrier)
@@ -1503,11 +1506,11 @@ static StripPlan<T> plan_strip(const Geom& g) {
     return p;
 }
 
-template <class T, bool BAL>
+template <class T, bool BAL, bool SL>
 static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t smem, cudaStream_t st) {
     static std::atomic<size_t> attr_bytes[kMaxDevices];     // per instantiation and device
     {
-        cudaError_t err = ensure_smem_attr((const void*)strip_conv_kernel<T, BAL>, smem, attr_bytes);
+        cudaError_t err = ensure_smem_attr((const void*)strip_conv_kernel<T, BAL, SL>, smem, attr_bytes);
         if (err != cudaSuccess) return err;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1538,7 +1541,7 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
         attr[cfg.numAttrs].val.cooperative = 1;
         cfg.numAttrs++;
     }
-    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL>, a);
+    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL, SL>, a);
 }
 
 template <class T>
@@ -1557,12 +1560,17 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     // CTA, so the SM holding the most units sets the kernel time): one CTA per resident
     // slot, equal-work channel ranges.  Measured at batch 32 (cfg5): -10..-13% at skew 1.32
     // (L0, L3), -5% (L4); at skew 1.16 between -5% (L7) and +4% (L12), hence the threshold.
+    // Re-measured on the round-2 kernel (flagged-encoding handling, slot parse): at skew 1.32 the
+    // stride-1 layers now lose (L0 125.0 vs 118.8 us, L4 124.9 vs 118.8) while stride 2 still
+    // gains (L3 182.3 vs 204.8), so stride-1 grids need skew >= 1.5.
     a.sk_ctas = 0;
     a.sk_strips = strips;
     a.sk_units = pl.ctas;
     const int nsm = sm_count();
     const double skew = (double)((pl.ctas + nsm - 1) / nsm) * nsm / (double)pl.ctas;
-    if (cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
+    const bool slots = a.sa_types || a.cscc;   // slot layouts: no balanced mode (one fewer instantiation)
+    const double skew_min = (g.sh > 1 || g.sw > 1) ? 1.2 : 1.5;
+    if (!slots && cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= skew_min) {
         int occ = 0;
         if (cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) != cudaSuccess) {
@@ -1577,8 +1585,9 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     if (getenv("SPC_PLAN_DEBUG"))
         fprintf(stderr, "strip plan: units %lld strips %d kblocks %d rt %d csplit %d cg %d sk_ctas %d smem %zu\n",
                 pl.ctas, strips, kblocks, a.rt, a.csplit, cg, a.sk_ctas, smem);
-    if (a.sk_ctas) return launch_strip<T, true>(a, dim3(a.sk_ctas, 1, 1), 1, smem, st);
-    return launch_strip<T, false>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
+    if (a.sk_ctas) return launch_strip<T, true, false>(a, dim3(a.sk_ctas, 1, 1), 1, smem, st);
+    if (slots) return launch_strip<T, false, true>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
+    return launch_strip<T, false, false>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
 }
 
 // Calls f(StripCfg<...>{}) for the strip configuration of this geometry; returns

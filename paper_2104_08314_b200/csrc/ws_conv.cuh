@@ -183,14 +183,17 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
             for (int i = p; i < min(T::NST, nchunks); i += T::NPROD) issue_taps(i);
         pdl_wait();
         if (lane == 0 && p == 0) probe_any(1);
-        const bool bad = *reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull;
+        // the encoding's flag word is loaded together with the side tables (in bounds whatever
+        // the flag), not ahead of them; a flagged encoding's streams are never read
+        const unsigned long long st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
         const long long ncb = (long long)n * g.C;
         // side tables of the CTA's channel range, once: ptr / DA offsets relative to the range start
-        const long long pbase = bad ? 0 : __ldg(a.cpo_off + ncb + c_begin);
-        const long long zbase = bad ? 0 : __ldg(a.cnz_off + ncb + c_begin);
+        const long long pbase = __ldg(a.cpo_off + ncb + c_begin);
+        const long long zbase = __ldg(a.cnz_off + ncb + c_begin);
         int* s_pof = s_coff;                       // [C range + 1]
         int* s_zof = s_cz;                         // [C range + 1]
-        for (int q = threadIdx.x; !bad && q <= c_end - c_begin; q += 32 * T::NPROD) {
+        const bool bad = st0 != 0ull;
+        for (int q = threadIdx.x; q <= c_end - c_begin; q += 32 * T::NPROD) {
             s_pof[q] = (int)(__ldg(a.cpo_off + ncb + c_begin + q) - pbase);
             s_zof[q] = (int)(__ldg(a.cnz_off + ncb + c_begin + q) - zbase);
         }

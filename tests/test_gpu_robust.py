@@ -2,6 +2,9 @@
 (spc_validate_encoding, SPC_ECORRUPT; SPEC.md:295 / :713) accepts every encoding the
 encoder emits and rejects corrupted ones; a convolution over an encoding the encoder
 flagged (capacity overflow) writes zeros instead of indexing incomplete streams."""
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -161,3 +164,33 @@ def test_last_conv_kernel_reports_the_launch():
         L.conv()
         torch.cuda.synchronize()
         assert spc.spc_last_conv_kernel() == kind, (name, spc.spc_last_conv_kernel())
+
+
+FLAGGED_BALANCED_CHILD = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from gpu_util import GpuLayer
+from synth import clustered_relu, he_normal, layer_desc
+d = layer_desc(12, 16, 56, 56, 64, 3, 3, 1, 1, 1, 1, 1, 1)
+x = clustered_relu(12, 16, 56, 56, 0.3, 91, 0.05, 0.1)
+L = GpuLayer(d, he_normal(64, 16, 3, 3, 91), caps=(100000, 1000, 1000))
+L.encode(torch.from_numpy(x).cuda())
+L.y.fill_(123.0)
+y = L.conv().cpu().numpy()
+print("zeros" if not y.any() else "nonzero")
+"""
+
+
+def test_flagged_encoding_through_balanced_mode():
+    """A flagged (overflowed) encoding on a shape that runs the balanced strip kernel
+    (persistent CTAs over equal-work channel ranges): every segment is walked as empty and
+    y = 0 -- round 2 regression: a flagged segment did not advance the CTA's work range, so
+    the kernel spun on the same segment.  Runs in a child process with a timeout."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", FLAGGED_BALANCED_CHILD, root], capture_output=True, text=True,
+                       timeout=180, env=dict(os.environ, SPC_PLAN_DEBUG="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "sk_ctas 0" not in r.stderr and "sk_ctas" in r.stderr, r.stderr[-2000:]   # the balanced mode ran
+    assert r.stdout.strip().endswith("zeros"), r.stdout
