@@ -1560,17 +1560,16 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     // CTA, so the SM holding the most units sets the kernel time): one CTA per resident
     // slot, equal-work channel ranges.  Measured at batch 32 (cfg5): -10..-13% at skew 1.32
     // (L0, L3), -5% (L4); at skew 1.16 between -5% (L7) and +4% (L12), hence the threshold.
-    // Re-measured on the round-2 kernel (flagged-encoding handling, slot parse): at skew 1.32 the
-    // stride-1 layers now lose (L0 125.0 vs 118.8 us, L4 124.9 vs 118.8) while stride 2 still
-    // gains (L3 182.3 vs 204.8), so stride-1 grids need skew >= 1.5.
+    // Re-measured on the round-2 kernel at skew 1.32 (conv us, balanced vs default grid, each
+    // layer's own density): L0 196.6 vs 204.8, L1 231.6 vs 249.9, L6 184.3 vs 196.6, L2 137.3 vs
+    // 133.1, L5 131.1 vs 129.0 (at rho 0.05 / 0.1 L0 and L4 lose ~5 %): the threshold stays.
     a.sk_ctas = 0;
     a.sk_strips = strips;
     a.sk_units = pl.ctas;
     const int nsm = sm_count();
     const double skew = (double)((pl.ctas + nsm - 1) / nsm) * nsm / (double)pl.ctas;
     const bool slots = a.sa_types || a.cscc;   // slot layouts: no balanced mode (one fewer instantiation)
-    const double skew_min = (g.sh > 1 || g.sw > 1) ? 1.2 : 1.5;
-    if (!slots && cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= skew_min) {
+    if (!slots && cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
         int occ = 0;
         if (cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) != cudaSuccess) {
