@@ -768,13 +768,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_serial_ms = e0.elapsed_time(e1)
 
-    # Pipelined form of the same steps (what a serving loop does): two buffer sets; per step,
+    # Pipelined form of the same steps (what a serving loop does): NB buffer sets; per step,
     # H2D on one stream, encode + conv on a second, D2H on a third, so step i's copies
     # overlap the neighbouring steps' compute.  One graph holds PIPE steps.
-    PIPE = 16
-    Ls = [R.layers[0], R.layers[1]]
-    xgs = [R.xs[0], R.xs[1]]
-    yhs = [yh, torch.empty(y.shape, dtype=torch.float32).pin_memory()]
+    PIPE = int(os.environ.get("BENCH_E2E_PIPE", "64"))   # steps per graph (fill / drain amortised)
+    NB = min(len(R.layers), int(os.environ.get("BENCH_E2E_NB", "2")))   # buffer sets in flight
+    Ls = [R.layers[b] for b in range(NB)]
+    xgs = [R.xs[b] for b in range(NB)]
+    yhs = [yh] + [torch.empty(y.shape, dtype=torch.float32).pin_memory() for _ in range(NB - 1)]
     s_h, s_c, s_d = (torch.cuda.Stream(device=dev) for _ in range(3))
     ev_h = [torch.cuda.Event() for _ in range(PIPE)]
     ev_c = [torch.cuda.Event() for _ in range(PIPE)]
@@ -785,16 +786,16 @@ def run_ours(args):
         for st_ in (s_h, s_c, s_d):
             st_.wait_stream(cs)
         for i in range(PIPE):
-            b = i & 1
+            b = i % NB
             with torch.cuda.stream(s_h):
-                if i >= 2:
-                    s_h.wait_event(ev_c[i - 2])      # xg[b] free: step i-2's encode read it
+                if i >= NB:
+                    s_h.wait_event(ev_c[i - NB])     # xg[b] free: step i-NB's encode read it
                 xgs[b].copy_(xh, non_blocking=True)
                 ev_h[i].record(s_h)
             with torch.cuda.stream(s_c):
                 s_c.wait_event(ev_h[i])
-                if i >= 2:
-                    s_c.wait_event(ev_d[i - 2])      # y[b] free: step i-2's D2H read it
+                if i >= NB:
+                    s_c.wait_event(ev_d[i - NB])     # y[b] free: step i-NB's D2H read it
                 Ls[b].forward(xgs[b], "cpo")
                 ev_c[i].record(s_c)
             with torch.cuda.stream(s_d):
@@ -928,8 +929,8 @@ def run_ours(args):
                                 "unit": "GB/s", "frac": enc_bytes / enc_s / 1e9 / hbm_gbs},
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": int(4 * x0.size),
                     "d2h_bytes_per_step": int(4 * d["N"] * d["K"] * Oh * Ow), "ms_per_step": e2e_ms / args.steps,
-                    "form": f"pipelined: H2D / encode+conv / D2H on three streams, {PIPE} steps per graph "
-                            "(fill and drain included), two buffer sets",
+                    "form": f"pipelined: H2D / encode+conv / D2H on three streams, {PIPE} steps per graph, {NB} buffer sets "
+                            "(fill and drain included)",
                     "serial": {"value": flops_step * args.steps * world / (e2e_serial_ms * 1e-3) / 1e9,
                                "ms_per_step": e2e_serial_ms / args.steps,
                                "form": "one step per graph: H2D, encode, conv, D2H in sequence"}},
