@@ -602,6 +602,16 @@ __device__ __forceinline__ void emit_omask(unsigned long long* omask, const Geom
             atomicOr(omask + ((long long)n * g.K + k) * g.Ow + ox0 + q, 1ull << oy);
 }
 
+// Balanced mode: wait for CTA b's "partial published" flag, bounded (a co-scheduled grid never
+// reaches the bound).  Returns false on a timeout; the kernel reports it (bit 2 of the encoding's
+// status word) once, after its segments -- the walk of the balanced strip kernel sits at its
+// register cap, and the 64-bit atomic inside the segment loop measurably spilled it.
+__device__ __forceinline__ bool sk_wait_flag(const unsigned* flag) {
+    unsigned spin = 0;
+    while (ld_acquire32(flag) == 0u && ++spin < (1u << 24)) __nanosleep(64);
+    return spin < (1u << 24);
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
@@ -734,7 +744,8 @@ __device__ int sk_start(const ConvArgs& a, int b) {
 //      cost multiply-adds (Alg. 2 convSpMv), with no indirect branches.
 // Epilogue: reduce the csplit warps of a row tile through smem, then the cg
 // CTAs of the cluster through distributed shared memory; ReLU; NKHW store.
-template <class T, bool BAL, bool SL = false>   // SL: stride-aware / CSCC slot parse (P1)
+template <class T, bool BAL, bool SL = false, bool OM = false>   // SL: stride-aware / CSCC slot parse (P1);
+// OM: NEXT-1 output row masks (only the fused conv + encode path carries their atomics)
 __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArgs a) {
     namespace cgrp = cooperative_groups;
     const Geom& g = a.g;
@@ -771,8 +782,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     // does not hold registers through the walk).  s_seg[0] advances after the first
     // barrier of each segment.
     __shared__ int s_seg[2];
+    __shared__ int s_flag;   // the encoding's status word != 0 (read by thread 0, published by a barrier)
     int t_next = 0;
-    bool bad = false;
     if constexpr (BAL) {
         if (threadIdx.x == 0) {
             s_seg[0] = sk_start<T>(a, blockIdx.x);
@@ -863,24 +874,37 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             probe(1);
             pdl_wait();
             probe(2);
+            // An encoding the encoder flagged (capacity overflow / wait timeout) is not read: every
+            // CTA sees the same word, writes zeros over each unit it touches and leaves -- no flag
+            // of the balanced mode is waited on, overlapping zero writes are harmless.  (A flag
+            // carried through the walk instead spilled the balanced kernel: measured.)
+            if (threadIdx.x == 0) s_flag = *reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull;
+            __syncthreads();
+            if (s_flag & 1) {
+                cp_async_wait_all();   // the prologue's tap copies land before the CTA leaves
+                for (;;) {
+                    const int rows = min(T::KB, g.K - kbase);
+                    float* yb0 = a.y + (long long)n * g.K * g.Oh * g.Ow;
+                    for (int i = threadIdx.x; i < rows * g.Oh * T::TX; i += nthreads) {
+                        const int xx = i % T::TX, r = i / T::TX, oy = r % g.Oh, kk = r / g.Oh;
+                        if (ox0 + xx < g.Ow) yb0[((long long)(kbase + kk) * g.Oh + oy) * g.Ow + ox0 + xx] = 0.f;
+                    }
+                    if constexpr (!BAL) break;
+                    __syncthreads();
+                    if (threadIdx.x == 0) s_seg[0] = t_next;
+                    __syncthreads();
+                    if (!next_segment(false)) break;
+                }
+                return;
+            }
         }
-        // an encoding the encoder flagged (capacity overflow / wait timeout) is not read: the
-        // unit's output is written as zeros (all threads read the same word).  The word is loaded
-        // together with the side tables (in bounds whatever the flag), not ahead of them.
-        unsigned long long st0 = 0ull;
-        if (first) st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
         int buf = 0;
-        if (c_begin < c_end) stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
-        if (st0 != 0ull && !bad) {
-            bad = true;
-            cp_async_wait_all();   // the prologue's tap copies land before smem is reused
+        if (c_begin < c_end) {
+            stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
+            if (BAL && threadIdx.x == 0) s_seg[0] = t_next;
+            stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
         }
-        // the balanced mode's range advances whatever the flag (a flagged encoding's segments are
-        // walked as empty: zero partials, published and summed as usual)
-        if (BAL && threadIdx.x == 0 && c_begin < c_end) s_seg[0] = t_next;
-        if (c_begin < c_end && !bad) stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
-        const int c_stop = bad ? c_begin : c_end;
-        for (int c0 = c_begin; c0 < c_stop; c0 += CHS, buf ^= 1) {
+        for (int c0 = c_begin; c0 < c_end; c0 += CHS, buf ^= 1) {
             const int chn = min(CHS, c_end - c0);
             const bool stage = !(dev_phase_mode() == 1 && !(first && c0 == c_begin));
             // ---- P0: taps (cp.async, with this chunk's prefetched ptr segments in flight); zero the windows
@@ -904,8 +928,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 const bool scatter = stage && !(dev_phase_mode() == 4 && !(first && c0 == c_begin));
                 int* fpre = s_scr;                      // [CH][32] column (slot) prefix within the channel
                 int* flo = fpre + T::CH * 32;           // [CH][32] DA offset of the column (slot)
-                int* fcb = flo + T::CH * 32;            // [CH][32] slot column base (stride-aware / CSCC)
-                int* ftot = fcb + T::CH * 32;           // [CH] NZEs of the channel in the window
+                int* fcb = flo + T::CH * 32;            // [CH][32] slot column base (stride-aware / CSCC; SL only)
+                int* ftot = SL ? fcb + T::CH * 32 : fcb; // [CH] NZEs of the channel in the window
                 // slots: window columns, or (partition, type) pairs (stride-aware), or submatrices (CSCC)
                 const int nsl = !SL ? T::WW
                               : a.cscc ? max(0, min(g.Ow - 1, (wx0 + T::WW - 1) / g.sw) - sa_slot_s_lo(g, wx0) + 1)
@@ -932,7 +956,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
                     fpre[j * 32 + lane] = (lane < nsl) ? pre : (1 << 30);
                     flo[j * 32 + lane] = lo;
-                    fcb[j * 32 + lane] = cb;
+                    if constexpr (SL) fcb[j * 32 + lane] = cb;
                     if (lane == 0) ftot[j] = tot;
                 }
                 if (scatter) __syncthreads();
@@ -1018,12 +1042,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     }
                     int tot;
                     const int pre = warp_exclusive_scan(hi - lo, &tot);
-                    int* spre = s_scr + warp * 96;
+                    int* spre = s_scr + warp * (SL ? 96 : 64);
                     int* slo = spre + 32;
                     int* scb = spre + 64;
                     spre[lane] = (lane < nsl) ? pre : (1 << 30);
                     slo[lane] = lo;
-                    scb[lane] = cb;
+                    if constexpr (SL) scb[lane] = cb;
                     const int lo0 = __shfl_sync(0xffffffffu, lo, 0);
                     const bool contig = __all_sync(0xffffffffu, lane >= nsl || hi == lo || lo == lo0 + pre);
                     __syncwarp();
@@ -1192,7 +1216,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     if (k >= g.K || oy >= g.Oh) continue;
                     float4 v = make_float4(accf[4 * i], accf[4 * i + 1], accf[4 * i + 2], accf[4 * i + 3]);
                     if (a.relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
-                    emit_omask(a.omask, g, n, k, oy, ox0, v);
+                    if constexpr (OM) emit_omask(a.omask, g, n, k, oy, ox0, v);
                     float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
                     if (vec_ok && ox0 + 3 < g.Ow) {
                         if (add)
@@ -1238,16 +1262,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                     int sb = sk_start<T>(a, blockIdx.x + 1);
                     for (int b = blockIdx.x + 1; b < a.sk_ctas && sb < uend; b++) {
                         const int sn = sk_start<T>(a, b + 1);
-                        if (sn > sb) {
-                            long long spin = 0;
-                            while (ld_acquire32(a.sk_flags + b) == 0u) {
-                                __nanosleep(64);
-                                if (++spin > (1ll << 24)) {   // bounded (co-scheduled grid: unreachable)
-                                    atomicOr(a.status, 4ull);
-                                    break;
-                                }
-                            }
-                        }
+                        if (sn > sb && !sk_wait_flag(a.sk_flags + b)) s_flag |= 2;   // bounded; reported below
                         sb = sn;
                     }
                 }
@@ -1315,7 +1330,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 const int c = ci / rows, row = ci % rows, kl = row & (T::KB - 1);   // kl = j*32 + lane
                 const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = (row / T::KB) * T::TY + c;
                 if (k >= g.K || oy >= g.Oh) continue;
-                emit_omask(a.omask, g, n, k, oy, ox0, sum);
+                if constexpr (OM) emit_omask(a.omask, g, n, k, oy, ox0, sum);
                 float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
                 if (vec_ok && ox0 + 3 < g.Ow) {
                     *reinterpret_cast<float4*>(dst) = sum;
@@ -1363,7 +1378,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             const int kl = row & (T::KB - 1), rr = row / T::KB;   // kl = j*32 + lane
             const int k = kbase + (kl & 31) * T::KPL + (kl >> 5), oy = rr * T::TY + c;   // chunk c = output row c
             if (k >= g.K || oy >= g.Oh) continue;
-            emit_omask(a.omask, g, n, k, oy, ox0, sum);
+            if constexpr (OM) emit_omask(a.omask, g, n, k, oy, ox0, sum);
             float* dst = yb + ((long long)k * g.Oh + oy) * g.Ow + ox0;
             if (vec_ok && ox0 + 3 < g.Ow) {
                 *reinterpret_cast<float4*>(dst) = sum;
@@ -1377,6 +1392,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         probe(9);
         if (a.cg > 1) cl.sync();
         probe(8);
+    }
+    if constexpr (BAL) {   // a balanced-mode wait that timed out (thread 0 set bit 1 of s_flag)
+        if (threadIdx.x == 0 && (s_flag & 2)) atomicOr(a.status, 4ull);
     }
 }
 
@@ -1443,8 +1461,10 @@ __global__ void __launch_bounds__(kGenWarps * 32) sparse_conv_generic_kernel(Con
 template <class T>
 static size_t strip_smem(const ConvArgs& a) {
     const int RT = a.rt, CS = a.csplit;
+    const bool slots = a.sa_types || a.cscc;   // the slot layouts' P1 keeps a column-base table too
+    const size_t scr = T::FLAT ? (size_t)T::CH * (slots ? 97 : 65) : (size_t)T::MAXW * (slots ? 96 : 64);
     const size_t main = (size_t)T::CH * T::RS * T::KB * 4 + (size_t)T::CH * RT * T::NCP * 4 +
-                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + (size_t)(T::FLAT ? T::CH * 97 : T::MAXW * 96) * 4;
+                        (size_t)2 * T::CH * a.pmax * 4 + (size_t)2 * (T::CW + 1) * 4 + scr * 4;
     const size_t epi = (size_t)RT * T::KB * (T::TY * T::TX) * 4 +
                        (CS > 1 ? (size_t)(CS - 1) * RT * T::NACC * 32 * 4 : 0);
     return std::max(main, epi);
@@ -1506,11 +1526,11 @@ static StripPlan<T> plan_strip(const Geom& g) {
     return p;
 }
 
-template <class T, bool BAL, bool SL>
+template <class T, bool BAL, bool SL, bool OM = false>
 static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t smem, cudaStream_t st) {
     static std::atomic<size_t> attr_bytes[kMaxDevices];     // per instantiation and device
     {
-        cudaError_t err = ensure_smem_attr((const void*)strip_conv_kernel<T, BAL, SL>, smem, attr_bytes);
+        cudaError_t err = ensure_smem_attr((const void*)strip_conv_kernel<T, BAL, SL, OM>, smem, attr_bytes);
         if (err != cudaSuccess) return err;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1541,7 +1561,7 @@ static cudaError_t launch_strip(const ConvArgs& a, dim3 grid, int cg, size_t sme
         attr[cfg.numAttrs].val.cooperative = 1;
         cfg.numAttrs++;
     }
-    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL, SL>, a);
+    return cudaLaunchKernelEx(&cfg, strip_conv_kernel<T, BAL, SL, OM>, a);
 }
 
 template <class T>
@@ -1569,7 +1589,8 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
     const int nsm = sm_count();
     const double skew = (double)((pl.ctas + nsm - 1) / nsm) * nsm / (double)pl.ctas;
     const bool slots = a.sa_types || a.cscc;   // slot layouts: no balanced mode (one fewer instantiation)
-    if (!slots && cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
+    const bool om = a.omask != nullptr;          // fused encode: no balanced mode either
+    if (!slots && !om && cg == 1 && a.scratch && a.sk_flags && balance_enabled() && pl.ctas > nsm && skew >= 1.2) {
         int occ = 0;
         if (cudaFuncSetAttribute(strip_conv_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, strip_conv_kernel<T, true>, 32 * a.rt * a.csplit, smem) != cudaSuccess) {
@@ -1586,6 +1607,7 @@ static cudaError_t run_strip(ConvArgs& a, cudaStream_t st) {
                 pl.ctas, strips, kblocks, a.rt, a.csplit, cg, a.sk_ctas, smem);
     if (a.sk_ctas) return launch_strip<T, true, false>(a, dim3(a.sk_ctas, 1, 1), 1, smem, st);
     if (slots) return launch_strip<T, false, true>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
+    if (om) return launch_strip<T, false, false, true>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
     return launch_strip<T, false, false>(a, dim3(strips, kblocks, g.N * cg), cg, smem, st);
 }
 
