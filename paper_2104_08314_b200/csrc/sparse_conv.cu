@@ -1618,7 +1618,7 @@ static cudaError_t visit_strip_cfg(const Geom& g, F&& f) {
     if (g.R == 3 && g.S == 3 && g.sh == 1 && g.sw == 1) {
         if (g.K <= 32 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 1, 1, 16, 32>{});
         if (g.K <= 64 && g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 32, true>{});
-        if (g.Oh <= 32) return f(StripCfg<3, 3, 1, 1, 4, 4, 4>{});
+        if (g.Oh <= 32) return f(StripCfg<3, 3, 1, 1, 4, 4, 4, 2, 8, 8>{});   // CH 8: CH 16 spills at 128 registers (L4 139 vs 147 us)
         if (g.Oh <= 64) return f(StripCfg<3, 3, 1, 1, 8, 4, 4, 1>{});
         if (g.Oh <= 128) return f(StripCfg<3, 3, 1, 1, 8, 4, 2, 1, 16, 16, true>{});   // up to 16 row tiles
     } else if (g.R == 5 && g.S == 5 && g.sh == 1 && g.sw == 1 && g.Oh <= 64) {
