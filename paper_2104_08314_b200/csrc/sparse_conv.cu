@@ -838,7 +838,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     // per chunk) and the ptr segments of the next chunk, prefetched during the walk.
     int cw0 = 0, cw1 = 0;
     long long cbase = 0, zbase = 0;
-    auto stage_window = [&](int c) {
+    // (pub: thread 0 also publishes the encoding's flag word, loaded before the side tables, through
+    // the same barrier)
+    auto stage_window = [&](int c, bool pub = false, unsigned long long st = 0ull) {
         const long long nc = (long long)n * g.C + c;
         cw0 = c;
         cw1 = min(c_end, c + T::CW);
@@ -848,6 +850,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             s_coff[i] = (int)(__ldg(a.cpo_off + nc + i) - cbase);
             s_cz[i] = (int)(__ldg(a.cnz_off + nc + i) - zbase);
         }
+        if (pub) s_flag = st != 0ull;
         __syncthreads();
     };
     auto stage_ptr = [&](int c0, int chn, int buf) {
@@ -874,13 +877,26 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             probe(1);
             pdl_wait();
             probe(2);
-            // An encoding the encoder flagged (capacity overflow / wait timeout) is not read: every
-            // CTA sees the same word, writes zeros over each unit it touches and leaves -- no flag
-            // of the balanced mode is waited on, overlapping zero writes are harmless.  (A flag
-            // carried through the walk instead spilled the balanced kernel: measured.)
-            if (threadIdx.x == 0) s_flag = *reinterpret_cast<volatile unsigned long long*>(a.status) != 0ull;
-            __syncthreads();
-            if (s_flag & 1) {
+        }
+        // An encoding the encoder flagged (capacity overflow / wait timeout) is not read.  Its word is
+        // loaded alongside the side tables (in bounds whatever the flag), not ahead of them.
+        //  * balanced mode: every CTA sees the same word, writes zeros over each unit it touches and
+        //    leaves -- no flag of the balanced mode is waited on, overlapping zero writes are
+        //    harmless (a flag carried through the walk spilled the balanced kernel: measured);
+        //  * default grid: the chunk loop is skipped and the epilogue writes the zero accumulators
+        //    (the early-exit form cost the default kernel ~2 us on cfg3-s2 / cfg4a: measured).
+        bool bad = false;
+        int buf = 0;
+        if constexpr (BAL) {
+            unsigned long long st0 = 0ull;
+            if (first && threadIdx.x == 0) st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
+            if (c_begin < c_end) {
+                stage_window(c_begin, first && threadIdx.x == 0, st0);   // (its barrier orders every thread's read of s_seg before the update)
+            } else if (first) {
+                if (threadIdx.x == 0) s_flag = st0 != 0ull;
+                __syncthreads();
+            }
+            if (first && (s_flag & 1)) {
                 cp_async_wait_all();   // the prologue's tap copies land before the CTA leaves
                 for (;;) {
                     const int rows = min(T::KB, g.K - kbase);
@@ -889,7 +905,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                         const int xx = i % T::TX, r = i / T::TX, oy = r % g.Oh, kk = r / g.Oh;
                         if (ox0 + xx < g.Ow) yb0[((long long)(kbase + kk) * g.Oh + oy) * g.Ow + ox0 + xx] = 0.f;
                     }
-                    if constexpr (!BAL) break;
                     __syncthreads();
                     if (threadIdx.x == 0) s_seg[0] = t_next;
                     __syncthreads();
@@ -897,14 +912,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
                 }
                 return;
             }
+            if (c_begin < c_end) {
+                if (threadIdx.x == 0) s_seg[0] = t_next;
+                stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
+            }
+        } else {
+            unsigned long long st0 = 0ull;
+            if (first) st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
+            if (c_begin < c_end) stage_window(c_begin);
+            if (st0 != 0ull) {
+                bad = true;
+                cp_async_wait_all();   // the prologue's tap copies land before smem is reused
+            }
+            if (c_begin < c_end && !bad) stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
         }
-        int buf = 0;
-        if (c_begin < c_end) {
-            stage_window(c_begin);   // (its barrier orders every thread's read of s_seg before the update)
-            if (BAL && threadIdx.x == 0) s_seg[0] = t_next;
-            stage_ptr(c_begin, min(CHS, c_end - c_begin), 0);
-        }
-        for (int c0 = c_begin; c0 < c_end; c0 += CHS, buf ^= 1) {
+        const int c_stop = bad ? c_begin : c_end;
+        for (int c0 = c_begin; c0 < c_stop; c0 += CHS, buf ^= 1) {
             const int chn = min(CHS, c_end - c0);
             const bool stage = !(dev_phase_mode() == 1 && !(first && c0 == c_begin));
             // ---- P0: taps (cp.async, with this chunk's prefetched ptr segments in flight); zero the windows
