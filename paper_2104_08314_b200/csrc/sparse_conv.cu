@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
     __shared__ int s_seg[2];
     __shared__ int s_flag;   // the encoding's status word != 0 (read by thread 0, published by a barrier)
     int t_next = 0;
+    bool bad = false;
     if constexpr (BAL) {
         if (threadIdx.x == 0) {
             s_seg[0] = sk_start<T>(a, blockIdx.x);
@@ -885,7 +886,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         //    harmless (a flag carried through the walk spilled the balanced kernel: measured);
         //  * default grid: the chunk loop is skipped and the epilogue writes the zero accumulators
         //    (the early-exit form cost the default kernel ~2 us on cfg3-s2 / cfg4a: measured).
-        bool bad = false;
         int buf = 0;
         if constexpr (BAL) {
             unsigned long long st0 = 0ull;
@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
             unsigned long long st0 = 0ull;
             if (first) st0 = *reinterpret_cast<volatile unsigned long long*>(a.status);
             if (c_begin < c_end) stage_window(c_begin);
-            if (st0 != 0ull) {
+            if (st0 != 0ull && !bad) {
                 bad = true;
                 cp_async_wait_all();   // the prologue's tap copies land before smem is reused
             }
