@@ -1187,6 +1187,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) strip_conv_kernel(ConvArg
         }
 
         probe(5);
+        // default grid: the next kernel may launch now (it waits for this grid's completion before
+        // reading anything written here; its CTAs start on SMs this grid leaves idle)
+        if constexpr (!BAL) pdl_trigger();
         // ---- epilogue: reduce the csplit warps of each row tile; partial -> part
         //      part = [RT*KB rows][TT positions], 16-byte chunks swizzled by (row & (NCH-1))
         //      so the lane-per-row float4 stores and the chunk-per-thread reads are conflict-free

@@ -435,6 +435,10 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
     }
 
     // ---- epilogue
+    // The next kernel (the next layer's or step's encoder) may launch now: it waits
+    // (griddepcontrol.wait) for this grid's completion before it reads anything we write, and its
+    // CTAs start on the SMs this grid leaves idle.
+    pdl_trigger();
     constexpr int TT = T::TY * T::TX, NCH = TT / 4;
     float* yb = a.y + (long long)n * g.K * g.Oh * g.Ow;
     const bool vec_ok = (g.Ow % 4) == 0;
