@@ -234,6 +234,15 @@ typedef enum {
 } spc_gemm;
 spc_status spc_set_im2col_gemm(spc_gemm gemm);   /* SPC_EINVAL for an unknown engine */
 spc_gemm spc_get_im2col_gemm(void);
+/* How sparse_conv_forward decodes a CPS encoding (K_w > 1; Alg. 4), process-wide:
+ * 0 (default) = a separate pass expands the CPS IN stream into CPO-form indices in the workspace,
+ * then the CPO convolution runs; 1 = on the layers the warp-specialised conv serves (14x14 @ 256,
+ * 7x7 @ 512, their stride-2 producers) its producer warps decode the CPS stream inline, per chunk
+ * of input channels (one launch; the other layers keep the expansion pass).  Both give identical
+ * outputs; the inline form measured slower on B200.  Initial value: the
+ * SPC_CPS_INLINE environment variable, else 0.  SPC_EINVAL for a value other than 0 / 1.  Host only. */
+spc_status spc_set_cps_inline(int32_t on);
+int32_t spc_get_cps_inline(void);
 /* The engine im2col_conv_forward runs for this layer under the current default (resolves
  * SPC_GEMM_AUTO and the tcgen05 engine's C*R*S % 4 fallback); host only. */
 spc_gemm spc_im2col_engine(const spc_conv_desc *d);

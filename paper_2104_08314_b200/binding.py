@@ -88,6 +88,10 @@ _lib.spc_set_im2col_gemm.argtypes = [ctypes.c_int]
 _lib.spc_set_im2col_gemm.restype = ctypes.c_int
 _lib.spc_get_im2col_gemm.argtypes = []
 _lib.spc_get_im2col_gemm.restype = ctypes.c_int
+_lib.spc_set_cps_inline.argtypes = [ctypes.c_int32]
+_lib.spc_set_cps_inline.restype = ctypes.c_int
+_lib.spc_get_cps_inline.argtypes = []
+_lib.spc_get_cps_inline.restype = ctypes.c_int32
 _lib.spc_im2col_engine.argtypes = [ctypes.c_void_p]
 _lib.spc_last_conv_kernel.argtypes = []
 _lib.spc_last_conv_kernel.restype = ctypes.c_int
@@ -102,7 +106,8 @@ _lib.spc_last_error.restype = ctypes.c_char_p
 _lib.spc_version.restype = ctypes.c_char_p
 
 EXPORTED = list(_sigs) + ["spc_fused_ws_bytes", "spc_select_ws_bytes", "spc_last_error", "spc_version", "spc_set_im2col_gemm",
-                          "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes", "spc_last_conv_kernel"]
+                          "spc_get_im2col_gemm", "spc_im2col_engine", "spc_im2col_ws_bytes", "spc_last_conv_kernel",
+                          "spc_set_cps_inline", "spc_get_cps_inline"]
 SPC_GEMM_SIMT, SPC_GEMM_CUBLAS_FP32, SPC_GEMM_CUBLAS_BF16X9, SPC_GEMM_CUBLAS_TF32, SPC_GEMM_TC_3XTF32 = 0, 1, 2, 3, 4
 SPC_GEMM_AUTO = 5
 GEMM_NAMES = {0: "SIMT FP32 FFMA (this library, 128x128 tiles)", 1: "cuBLAS FP32 (CUBLAS_COMPUTE_32F)",
@@ -121,6 +126,16 @@ def spc_set_im2col_gemm(gemm: int) -> None:
 
 def spc_get_im2col_gemm() -> int:
     return int(_lib.spc_get_im2col_gemm())
+
+
+def spc_set_cps_inline(on: bool) -> None:
+    st = _lib.spc_set_cps_inline(int(bool(on)))
+    if st != SPC_OK:
+        raise SpcError(st, "spc_set_cps_inline")
+
+
+def spc_get_cps_inline() -> bool:
+    return bool(_lib.spc_get_cps_inline())
 
 
 def spc_im2col_ws_bytes(d: dict) -> int:

@@ -10,6 +10,14 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
+// CPS decode form of sparse_conv_forward (spc_set_cps_inline): 0 = expansion pass, 1 = inline
+static std::atomic<int32_t> g_cps_inline{[] {
+    const char* v = getenv("SPC_CPS_INLINE");
+    return (v && atoi(v) == 1) ? 1 : 0;
+}()};
+
 namespace spc {
 size_t enc_smem_bytes(const Geom& g);
 const char* validate_reason(int code);
@@ -215,15 +223,6 @@ spc_status conv_impl(const spc_conv_desc* d, const spc_encoding* enc, const floa
         }
         return cuda_status(spc::launch_sa_conv(g, enc, w_packed, y, fuse_relu, st), "sparse_conv (stride-aware)");
     }
-    const int32_t* in_cpo = nullptr;
-    if (enc->algo == SPC_ALGO_CPS && d->S > 1) {
-        spc::WsLayout L = spc::ws_layout(g);
-        if (!ws || ws_bytes < L.total) return fail(SPC_EINVAL, "CPS convolution needs the workspace");
-        int32_t* buf = reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.cps_in);
-        spc_status r = cuda_status(spc::launch_cps_expand(g, enc, buf, st), "cps_expand");
-        if (r != SPC_OK) return r;
-        in_cpo = buf;
-    }
     float* scratch = nullptr;
     size_t scratch_bytes = 0;
     if (ws) {
@@ -232,6 +231,22 @@ spc_status conv_impl(const spc_conv_desc* d, const spc_encoding* enc, const floa
             scratch = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + L.scratch);
             scratch_bytes = L.total - L.scratch;
         }
+    }
+    const int32_t* in_cpo = nullptr;
+    if (enc->algo == SPC_ALGO_CPS && d->S > 1) {
+        spc::WsLayout L = spc::ws_layout(g);
+        if (!ws || ws_bytes < L.total) return fail(SPC_EINVAL, "CPS convolution needs the workspace");
+        int32_t* buf = reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.cps_in);
+        // the warp-specialised conv decodes the CPS stream itself (Alg. 4 inline, one launch);
+        // the other conv kernels read CPO-form indices expanded by a separate pass
+        if (g_cps_inline.load(std::memory_order_relaxed)) {
+            const cudaError_t ce = spc::launch_sparse_conv(g, enc, buf, w_packed, y, fuse_relu, scratch, scratch_bytes,
+                                                           st, omask, 0, 0, true);
+            if (ce != cudaErrorNotSupported) return cuda_status(ce, "sparse_conv (CPS inline)");
+        }
+        spc_status r = cuda_status(spc::launch_cps_expand(g, enc, buf, st), "cps_expand");
+        if (r != SPC_OK) return r;
+        in_cpo = buf;
     }
     return cuda_status(spc::launch_sparse_conv(g, enc, in_cpo, w_packed, y, fuse_relu, scratch, scratch_bytes, st, omask),
                        "sparse_conv");
@@ -310,6 +325,13 @@ spc_status spc_set_im2col_gemm(spc_gemm gemm) {
 }
 
 spc_gemm spc_get_im2col_gemm(void) { return (spc_gemm)spc::gemm_engine(); }
+
+spc_status spc_set_cps_inline(int32_t on) {
+    if (on != 0 && on != 1) return fail(SPC_EINVAL, "spc_set_cps_inline: 0 or 1");
+    g_cps_inline.store(on);
+    return SPC_OK;
+}
+int32_t spc_get_cps_inline(void) { return g_cps_inline.load(); }
 
 int spc_last_conv_kernel(void) { return spc::last_conv_kernel(); }
 

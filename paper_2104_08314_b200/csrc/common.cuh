@@ -255,7 +255,7 @@ int last_conv_kernel();   // sparse_conv.cu: kernel of this thread's last sparse
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
                                cudaStream_t st, unsigned long long* omask = nullptr, unsigned sa_types = 0,
-                               int cscc = 0);
+                               int cscc = 0, bool cps_inline = false);
 cudaError_t launch_im2col(const Geom& g, const float* x, float* L, cudaStream_t st);
 cudaError_t launch_gemm(const Geom& g, const float* w, const float* L, float* y, int relu, cudaStream_t st,
                         float* extra = nullptr, size_t extra_bytes = 0);   // extra: workspace beyond the lowered matrix

@@ -541,6 +541,11 @@ struct ConvArgs {
     int sk_ctas;          // balanced mode: persistent CTAs (0 = one CTA per unit x cluster rank)
     int sk_strips;        // balanced mode: column strips per image (unit = (k-block, image, strip))
     long long sk_units;   // balanced mode: strips x images x k-blocks
+    // CPS decoded inside the warp-specialised conv (Alg. 4): cps_in = the CPS
+    // IN stream, cin_off = its per-channel offsets; `in` is then the workspace buffer a chunk too
+    // large for the producers' shared-memory stage is decoded into (null: CPO-form `in`)
+    const int32_t* __restrict__ cps_in;
+    const int64_t* __restrict__ cin_off;
 };
 
 // Strip-kernel configuration: a CTA owns a column strip of TX output columns and
@@ -1696,8 +1701,11 @@ int last_conv_kernel() { return t_last_conv_kernel; }
 
 cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32_t* in_override,
                                const float* w_packed, float* y, int relu, float* scratch, size_t scratch_bytes,
-                               cudaStream_t st, unsigned long long* omask, unsigned sa_types, int cscc) {
+                               cudaStream_t st, unsigned long long* omask, unsigned sa_types, int cscc,
+                               bool cps_inline) {
     ConvArgs a;
+    a.cps_in = cps_inline ? e->in : nullptr;
+    a.cin_off = cps_inline ? e->chan_in_off : nullptr;
     a.g = g;
     a.ptr = e->ptr;
     a.da = e->da;
@@ -1730,7 +1738,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
     a.pmax = (g.S == 1) ? (1 + g.Ow1) : (3 + (g.S - 1) * (1 + g.Ow1));
     if (sa_types || cscc) a.pmax = std::max(a.pmax, g.S * (1 + g.Ow));
     cudaError_t err = cudaErrorNotSupported;
-    if (!conv_v1_forced()) err = visit_tc_cfg(g, [&](auto cfg) { return run_tc<decltype(cfg)>(a, st); });
+    if (!conv_v1_forced() && !cps_inline) err = visit_tc_cfg(g, [&](auto cfg) { return run_tc<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) {
         t_last_conv_kernel = 3;
         return err;
@@ -1740,6 +1748,7 @@ cudaError_t launch_sparse_conv(const Geom& g, const spc_encoding* e, const int32
         t_last_conv_kernel = 2;
         return err;
     }
+    if (cps_inline) return cudaErrorNotSupported;   // only the ws kernel decodes CPS inline
     err = visit_strip_cfg(g, [&](auto cfg) { return run_strip<decltype(cfg)>(a, st); });
     if (err != cudaErrorNotSupported) {
         t_last_conv_kernel = 1;

@@ -57,12 +57,12 @@ struct WsCfg {
 
 // shared-memory carve-up (host and device agree through this)
 struct WsSmem {
-    size_t w, val, msk, pbuf, pre, lo, tot, cb, coff, cz, bars, total;
+    size_t w, val, msk, pbuf, pre, lo, tot, cb, coff, cz, cq, dec, bars, total;
     int pstride;   // ints of the ptr part of one producer buffer
     int bstride;   // bytes of one producer buffer: ptr | DA | IN
 };
 template <class T>
-__host__ __device__ inline WsSmem ws_smem_layout(int RT, int pmax, int crange) {
+__host__ __device__ inline WsSmem ws_smem_layout(int RT, int pmax, int crange, bool cps = false) {
     WsSmem L;
     L.pstride = (int)align_up((size_t)T::CH * pmax + 8, 4);
     L.bstride = (int)((size_t)L.pstride * 4 + (size_t)2 * (T::DCAP + 8) * 4);
@@ -76,7 +76,9 @@ __host__ __device__ inline WsSmem ws_smem_layout(int RT, int pmax, int crange) {
     L.cb = L.tot + (size_t)T::NPROD * T::CH * 4;                                  // [NPROD][CH][32] slot column base
     L.coff = L.cb + (size_t)T::NPROD * T::CH * 32 * 4;                            // [crange+1] ptr offsets (rel)
     L.cz = L.coff + (size_t)(crange + 1) * 4;                                     // [crange+1] DA offsets (rel)
-    L.bars = align_up(L.cz + (size_t)(crange + 1) * 4 + 16, 16);                 // full, empty [NST], pbar [NPROD][2]
+    L.cq = L.cz + (size_t)(crange + 1) * 4;                                       // [crange+1] CPS IN offsets (rel)
+    L.dec = align_up(L.cq + (cps ? (size_t)(crange + 1) * 4 : 0), 16);            // [NPROD][DCAP+8] decoded CPS IN
+    L.bars = align_up(L.dec + (cps ? (size_t)T::NPROD * (T::DCAP + 8) * 4 : 0) + 16, 16);   // full, empty [NST], pbar [NPROD][2]
     L.total = L.bars + (size_t)(2 * T::NST + 2 * T::NPROD) * 8 + 64;
     return L;
 }
@@ -113,7 +115,8 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
     const int kvalid = min(T::KBC, g.K - kbase);      // output channels of this CTA that exist
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const WsSmem L = ws_smem_layout<T>(RT, a.pmax, cper);
+    const bool cps = a.cps_in != nullptr;   // CPS stream decoded by the producers (Alg. 4)
+    const WsSmem L = ws_smem_layout<T>(RT, a.pmax, cper, cps);
     float* s_w = reinterpret_cast<float*>(smem_raw + L.w);
     float* s_val = reinterpret_cast<float*>(smem_raw + L.val);
     unsigned* s_msk = reinterpret_cast<unsigned*>(smem_raw + L.msk);
@@ -193,9 +196,12 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
         int* s_pof = s_coff;                       // [C range + 1]
         int* s_zof = s_cz;                         // [C range + 1]
         const bool bad = st0 != 0ull;
+        const long long qbase = cps ? __ldg(a.cin_off + ncb + c_begin) : 0;
+        int* s_qof = reinterpret_cast<int*>(smem_raw + L.cq);   // [C range + 1] (CPS only)
         for (int q = threadIdx.x; q <= c_end - c_begin; q += 32 * T::NPROD) {
             s_pof[q] = (int)(__ldg(a.cpo_off + ncb + c_begin + q) - pbase);
             s_zof[q] = (int)(__ldg(a.cnz_off + ncb + c_begin + q) - zbase);
+            if (cps) s_qof[q] = (int)(__ldg(a.cin_off + ncb + c_begin + q) - qbase);
         }
         producer_sync();
         int* wpre = fpre + p * T::CH * 32;         // this warp's column tables
@@ -215,21 +221,21 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
             const long long pa = P0 & ~3ll, za = Z0 & ~3ll;
             const long long pn = ((P1 - pa) >> 2) << 2, zn = ((Z1 - za) >> 2) << 2;
             const bool fits = (Z1 - za) <= T::DCAP + 4;
+            // IN: the CPO-form stream at the DA positions, or the CPS stream (never longer than DA)
+            const long long Q0 = cps ? qbase + s_qof[r0] : za, Q1 = cps ? qbase + s_qof[r0 + chn] : Z1;
+            const long long qa = Q0 & ~3ll, qn = ((Q1 - qa) >> 2) << 2;
+            const int32_t* isrc = cps ? a.cps_in : a.in;
             int* dp = pb_ptr(b);
             if (lane == 0) {
                 fence_proxy_async();   // generic reads of this buffer (two chunks ago) before the copies
-                mbar_expect_tx(&pbar[2 * p + b], (unsigned)(4 * (pn + (fits ? 2 * zn : 0))));
+                mbar_expect_tx(&pbar[2 * p + b], (unsigned)(4 * (pn + (fits ? zn + qn : 0))));
                 if (pn > 0) bulk_g2s(dp, a.ptr + pa, (unsigned)(pn * 4), &pbar[2 * p + b]);
-                if (fits && zn > 0) {
-                    bulk_g2s(pb_da(b), a.da + za, (unsigned)(zn * 4), &pbar[2 * p + b]);
-                    bulk_g2s(pb_in(b), a.in + za, (unsigned)(zn * 4), &pbar[2 * p + b]);
-                }
+                if (fits && zn > 0) bulk_g2s(pb_da(b), a.da + za, (unsigned)(zn * 4), &pbar[2 * p + b]);
+                if (fits && qn > 0) bulk_g2s(pb_in(b), isrc + qa, (unsigned)(qn * 4), &pbar[2 * p + b]);
             }
             if (pa + pn + lane < P1) dp[pn + lane] = __ldg(a.ptr + pa + pn + lane);
-            if (fits && za + zn + lane < Z1) {
-                pb_da(b)[zn + lane] = __ldg(a.da + za + zn + lane);
-                pb_in(b)[zn + lane] = __ldg(a.in + za + zn + lane);
-            }
+            if (fits && za + zn + lane < Z1) pb_da(b)[zn + lane] = __ldg(a.da + za + zn + lane);
+            if (fits && qa + qn + lane < Q1) pb_in(b)[qn + lane] = __ldg(isrc + qa + qn + lane);
         };
         if (!bad && p < nchunks) prefetch(p, 0);
         int k = 0;   // this warp's chunk counter (buffer k & 1)
@@ -260,7 +266,8 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
             const bool fits = (Z1 - za) <= T::DCAP + 4;
             const int* sp = pb_ptr(b);
             const float* sda = pb_da(b) + (Z0 - za);   // DA / IN of the chunk's first channel
-            const int* sin = pb_in(b) + (Z0 - za);
+            int* const sdec = reinterpret_cast<int*>(smem_raw + L.dec) + p * (T::DCAP + 8);
+            const int* sin = cps ? sdec : pb_in(b) + (Z0 - za);
             // masks of this stage start empty; the window VALUES are never zeroed -- a consumer only
             // reads a window slot whose mask bit the scatter below set
             unsigned* mk = s_msk + s * msk_stage;
@@ -286,6 +293,9 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                         } else {
                             parse_dir<T::S>(g, seg, d);
                             if (!d.npc && col < T::WW) column_range_s<T::S>(g, seg, d, wx0 + col, lo, hi);
+                            // CPS: DA start of the overlapK_w block (the entries before it are 1:1)
+                            if (cps && col == 0)
+                                wcb[j * 32 + 31] = (d.npc || d.pos[T::S - 1] < 0) ? (1 << 30) : d.da[T::S - 1];
                         }
                     }
                     int inc = hi - lo;
@@ -303,6 +313,66 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                 }
             }
             __syncwarp();
+            if (cps) {
+                // (a') Alg. 4 over the chunk's CPS IN entries flattened across its
+                //      channels (their segments are contiguous): entries below a channel's overlapK_w
+                //      block are 1:1 with DA; inside it a negative entry is a singleton at -e, a
+                //      non-negative one an index followed by its pattern P (rows e + S*(bit - lowest
+                //      bit)).  Indices and patterns alternate after the last 1:1 / negative entry (the
+                //      role is the parity of the distance to it, carried across 32-entry slices); NZE
+                //      counts scanned give the DA positions.  Output: CPO-form indices at the chunk's
+                //      DA positions, in shared memory when the chunk was staged, else in the
+                //      workspace buffer `a.in`.
+                const long long Q0 = qbase + s_qof[r0];
+                const int* qsrc = fits ? pb_in(b) + (int)(Q0 & 3ll) : a.cps_in + Q0;
+                int* zdst = fits ? sdec : const_cast<int*>(a.in) + Z0;
+                const int nq = s_qof[r0 + chn] - s_qof[r0];
+                const int qj = (lane < chn) ? s_qof[r0 + lane] - s_qof[r0] : (1 << 30);
+                const int dmj = (lane < chn) ? wcb[lane * 32 + 31] : 0;
+                int dpos = 0;
+                bool carry = false;
+                for (int q = 0; q < nq; q += 32) {
+                    const int i = q + lane;
+                    const bool valid = i < nq;
+                    const int e = valid ? qsrc[i] : -1;
+                    int j = 0;
+#pragma unroll
+                    for (int step = T::CH / 2; step > 0; step >>= 1) {
+                        const int cand = j + step;
+                        const int cv = __shfl_sync(0xffffffffu, qj, cand & 31);
+                        if (cand < chn && cv <= i) j = cand;
+                    }
+                    const int rel = i - __shfl_sync(0xffffffffu, qj, j);
+                    const int dm = __shfl_sync(0xffffffffu, dmj, j);
+                    const bool one = valid && rel < dm;
+                    const bool brk = valid && (one || e < 0);
+                    const unsigned before = __ballot_sync(0xffffffffu, brk) & lanemask_lt();
+                    const int r = before ? (32 - __clz(before)) : 0;
+                    const bool base_pat = (r == 0) ? carry : false;
+                    const bool nonneg = valid && !brk;
+                    const bool is_pat = nonneg && (base_pat ^ (((lane - r) & 1) != 0));
+                    const bool is_idx = nonneg && !is_pat;
+                    int nxt = __shfl_down_sync(0xffffffffu, e, 1);
+                    if (lane == 31) nxt = (i + 1 < nq) ? qsrc[i + 1] : -1;
+                    const int cnt = brk ? 1 : (is_idx ? __popc(nxt & 0xF) : 0);
+                    int tot;
+                    const int o = dpos + warp_exclusive_scan(cnt, &tot);
+                    if (brk) {
+                        zdst[o] = one ? e : -e;
+                    } else if (is_idx) {
+                        const unsigned pm = (unsigned)nxt & 0xFu;
+                        const int b0 = __ffs(pm) - 1;
+                        int u = 0;
+#pragma unroll
+                        for (int bb = 0; bb < 4; bb++)
+                            if ((pm >> bb) & 1u) zdst[o + u++] = e + T::S * (bb - b0);
+                    }
+                    carry = __shfl_sync(0xffffffffu, is_idx, 31);
+                    dpos += tot;
+                }
+                if (!fits) __threadfence_block();
+                __syncwarp();
+            }
             // (b) the chunk's NZEs flattened across its channels (staged DA / IN, or global memory
             //     for a chunk beyond DCAP): value into every row tile window holding the row, and the
             //     window's occupancy bit (shared-memory atomic OR)
@@ -340,7 +410,8 @@ __global__ void __maxnreg__(T::MAXREG) ws_conv_kernel(WsArgs wa) {
                                 e[u] = sin[zr + idx];
                                 v[u] = sda[zr + idx];
                             } else {
-                                e[u] = __ldg(a.in + Z0 + zr + idx);
+                                // (decoded by this warp just above when CPS: L2 loads, not the nc path)
+                                e[u] = cps ? __ldcg(a.in + Z0 + zr + idx) : __ldg(a.in + Z0 + zr + idx);
                                 v[u] = __ldg(a.da + Z0 + zr + idx);
                             }
                             pos[u] = j * RT + jc * 65536;          // window (j, 0) and column jc
@@ -523,7 +594,7 @@ struct WsPlan {
 };
 
 template <class T>
-static bool plan_ws(const Geom& g, int pmax, WsPlan<T>& p) {
+static bool plan_ws(const Geom& g, int pmax, WsPlan<T>& p, bool cps = false) {
     p.strips = (g.Ow + T::TX - 1) / T::TX;
     p.RT = (g.Oh + T::TY - 1) / T::TY;
     p.ncons = p.RT * T::KG;
@@ -538,7 +609,7 @@ static bool plan_ws(const Geom& g, int pmax, WsPlan<T>& p) {
     p.cg = 1;
     for (int cg = 2; cg <= 8; cg *= 2)
         if (p.units * cg <= sms && g.C >= 2 * cg * T::CH) p.cg = cg;
-    p.smem = ws_smem_layout<T>(p.RT, pmax, (g.C + p.cg - 1) / p.cg).total;
+    p.smem = ws_smem_layout<T>(p.RT, pmax, (g.C + p.cg - 1) / p.cg, cps).total;
     if (p.smem > 227 * 1024) return false;
     p.scratch_bytes = (p.cg > 1) ? (size_t)p.units * p.cg * p.RT * T::KBC * T::TY * T::TX * 4 : 0;
     return true;
@@ -553,10 +624,10 @@ static cudaError_t run_ws(ConvArgs& a, cudaStream_t st) {
     static const int ws_slots = [] { const char* v = getenv("SPC_WS_SLOTS"); return v ? atoi(v) : 1; }();
     if (a.cscc || (a.sa_types && !ws_slots)) return cudaErrorNotSupported;
     WsPlan<T> p;
-    if (!plan_ws<T>(g, a.pmax, p)) return cudaErrorNotSupported;
+    if (!plan_ws<T>(g, a.pmax, p, a.cps_in != nullptr)) return cudaErrorNotSupported;
     if (p.cg > 1 && (!a.scratch || a.scratch_bytes < p.scratch_bytes)) {          // no scratch: no split
         p.cg = 1;
-        p.smem = ws_smem_layout<T>(p.RT, a.pmax, g.C).total;   // one CTA's side tables cover every channel
+        p.smem = ws_smem_layout<T>(p.RT, a.pmax, g.C, a.cps_in != nullptr).total;   // one CTA's side tables cover every channel
         if (p.smem > 227 * 1024) return cudaErrorNotSupported;
     }
     WsArgs wa;

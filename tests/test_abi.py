@@ -107,3 +107,18 @@ def test_im2col_engine_resolution(lib):
             lib.spc_set_im2col_gemm(6)
     finally:
         lib.spc_set_im2col_gemm(prev)
+
+
+def test_cps_inline_toggle(lib):
+    """spc_set_cps_inline: 0 / 1 accepted and read back, anything else SPC_EINVAL (host only)."""
+    prev = lib.spc_get_cps_inline()
+    try:
+        for on in (True, False):
+            lib.spc_set_cps_inline(on)
+            assert lib.spc_get_cps_inline() is on
+        raw = ctypes.CDLL(lib.LIB_PATH)
+        raw.spc_set_cps_inline.argtypes = [ctypes.c_int32]
+        assert raw.spc_set_cps_inline(2) == lib.SPC_EINVAL
+        assert lib.spc_get_cps_inline() is False
+    finally:
+        lib.spc_set_cps_inline(prev)

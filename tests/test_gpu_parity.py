@@ -425,16 +425,26 @@ def test_tc_gemm_3xtf32_shapes(oracle_mod, shape):
     (1, 300, 14, 14, 256, 1),    # many chunks (NST-stage ring wraps several times), ragged last chunk
 ])
 @pytest.mark.parametrize("rho", [0.0, 0.07, 0.4, 1.0])
-def test_ws_conv_integer_exact(oracle_mod, shape, rho):
+@pytest.mark.parametrize("cps", [False, "expand", "inline"])
+def test_ws_conv_integer_exact(oracle_mod, shape, rho, cps):
     """The warp-specialised conv (ws_conv.cuh) against the oracle's Eq. 1 on integer data:
-    every output element exactly equal (ragged chunks, all-zero and dense maps, cluster split)."""
+    every output element exactly equal (ragged chunks, all-zero and dense maps, cluster split).
+    CPS encodings: "expand" = the separate Alg. 4 expansion pass, "inline" = the producers decode
+    the CPS stream themselves (Alg. 4) -- from shared memory, or through the
+    workspace for chunks beyond the stage (rho = 1.0)."""
     N, C, H, W, K, s = shape
     d = layer_desc(N, C, H, W, K, 3, 3, s, s, 1, 1, 1, 1)
     x = int_map(N, C, H, W, rho, 1000 + C)
     x[:, ::7] = 0                                   # some NPC channels
     w = int_weights(K, C, 3, 3, 7)
     L = GpuLayer(d, w)
-    L.encode(torch.from_numpy(x).cuda())
-    y = L.conv().cpu().numpy()
+    L.encode(torch.from_numpy(x).cuda(), bool(cps))
+    prev = spc.spc_get_cps_inline()
+    try:
+        spc.spc_set_cps_inline(cps == "inline")
+        y = L.conv().cpu().numpy()
+    finally:
+        spc.spc_set_cps_inline(prev)
+    assert spc.spc_last_conv_kernel() == 2          # the warp-specialised kernel ran
     ref = oracle_mod.direct_conv(d, x, w)
     assert np.array_equal(y, ref.astype(np.float32)), np.abs(y - ref).max()
